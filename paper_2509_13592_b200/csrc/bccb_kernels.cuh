@@ -1,0 +1,461 @@
+// Pass kernels of the fused BCCB Gram iteration (sm_100a).
+//
+// One solver iteration = two launches:
+//   rows_kernel  (pass A, one L1-line per team): band inverse of V -> g, fused solver
+//                epilogue (gradient step + complex soft-threshold + FISTA momentum or
+//                ADMM z/v update + non-finite flag), band forward of the next operator
+//                input -> U.
+//   cols_kernel  (pass B, one L2-line per (snapshot, k1) team): band forward of U,
+//                spectral multiply-add  Y = D*X + P*Bhat  on the K2 x K1 box, band
+//                inverse -> V.
+// Intermediates U, V are [B][K1][L2] complex64 (transposed so pass B lines are
+// contiguous); Bhat / D / P boxes are [.][K1][K2].  The full-grid state never
+// leaves its [B][L2][L1] layout.  See DESIGN.md for the byte model.
+#pragma once
+#include "band_fft.cuh"
+
+namespace bccb {
+
+struct Geo {
+  int L1, L2;
+  long long rows;  // total lines in this launch
+  int TR;          // lines per CTA
+  int do_inv, do_fwd;
+};
+
+// ------------------------------------------------------------------ epilogues
+// Every epilogue provides
+//   float2 load(pos, b)          : operator input x_t from the current state (first pass)
+//   float2 update(pos, b, g)     : consume g = (ifft2 part) at pos, update the state,
+//                                  return the next operator input x_{t+1}
+// `pos` is the flat index b*L + l2*L1 + l1; `b` the snapshot.
+
+// Plain input (matvec / spectrum of a user vector).  update() returns
+// out = alpha*x + scale*g; the kernel stores it and (optionally) reduces max|out|
+// per snapshot with one atomic per (warp, snapshot) group.
+struct EpiVector {
+  const float2* __restrict__ in;   // may be null when alpha == 0
+  float2* __restrict__ out;        // may be null (only maxabs wanted)
+  float* __restrict__ maxabs;      // may be null
+  float alpha, scale;
+  __device__ __forceinline__ float2 load(long long pos, int) const { return in[pos]; }
+  __device__ __forceinline__ float2 update(long long pos, int, float2 g) const {
+    float2 o = make_float2(scale * g.x, scale * g.y);
+    if (alpha != 0.f) {
+      const float2 x = in[pos];
+      o.x = fmaf(alpha, x.x, o.x);
+      o.y = fmaf(alpha, x.y, o.y);
+    }
+    if (out) out[pos] = o;
+    return o;
+  }
+};
+
+// max over lanes that share the same snapshot b, then one atomicMax per group.
+// |.| >= 0, so IEEE bit patterns order like unsigned ints (NaN sorts high).
+__device__ __forceinline__ void group_atomic_max(float* maxabs, int b, float m) {
+  const unsigned act = __activemask();
+  const unsigned grp = __match_any_sync(act, b);
+  const unsigned v = __reduce_max_sync(grp, __float_as_uint(m));
+  if ((threadIdx.x & 31) == (__ffs(grp) - 1))
+    atomicMax(reinterpret_cast<unsigned int*>(maxabs) + b, v);
+}
+
+// ISTA (momentum=false) and FISTA (momentum=true).
+// State: c (complex128) and, for FISTA, d = c_t - c_{t-1} (complex64).
+// x_t = c_t + beta_t * d_t ;  w = a*x_t + g (+ extra_scale*extra) ;
+// c_{t+1} = S_kappa(w) ;  d_{t+1} = c_{t+1} - c_t ;  x_{t+1} = c_{t+1} + beta_{t+1} d_{t+1}.
+// reference: pkg/src/bccblasso/solvers.py:245-249 (prox step), 131-145 (soft threshold),
+//            311-355 (FISTA loop), 252-291 (ISTA loop), 222-224 (finite check).
+struct EpiFista {
+  double2* c;
+  float2* d;
+  const float2* __restrict__ extra;
+  const double* __restrict__ tau;  // [B]
+  int* first_bad;                  // [B]
+  double a, kscale, extra_scale, beta_cur, beta_next;
+  int it, momentum;
+
+  __device__ __forceinline__ float2 load(long long pos, int) const {
+    double2 cc = c[pos];
+    if (momentum) {
+      const float2 dd = d[pos];
+      cc.x = __fma_rn(beta_cur, (double)dd.x, cc.x);
+      cc.y = __fma_rn(beta_cur, (double)dd.y, cc.y);
+    }
+    return make_float2((float)cc.x, (float)cc.y);
+  }
+  __device__ __forceinline__ float2 step(double2 cc, float2 dd, float2 g, float2 e, int b,
+                                         double2& cn, float2& dn) const {
+    double xr = cc.x, xi = cc.y;
+    if (momentum) {
+      xr = __fma_rn(beta_cur, (double)dd.x, xr);
+      xi = __fma_rn(beta_cur, (double)dd.y, xi);
+    }
+    double wr = __fma_rn(a, xr, (double)g.x);
+    double wi = __fma_rn(a, xi, (double)g.y);
+    if (extra) {
+      wr = __fma_rn(extra_scale, (double)e.x, wr);
+      wi = __fma_rn(extra_scale, (double)e.y, wi);
+    }
+    if (!isfinite(wr) || !isfinite(wi)) atomicMin(first_bad + b, it);
+    const double kap = kscale * tau[b];
+    const double m2 = wr * wr + wi * wi;
+    if (m2 <= kap * kap) {
+      cn.x = 0.0;
+      cn.y = 0.0;
+    } else {
+      const double f = 1.0 - kap / sqrt(m2);
+      cn.x = wr * f;
+      cn.y = wi * f;
+    }
+    if (momentum) {
+      dn.x = (float)(cn.x - cc.x);
+      dn.y = (float)(cn.y - cc.y);
+      const double nx = __fma_rn(beta_next, (double)dn.x, cn.x);
+      const double ny = __fma_rn(beta_next, (double)dn.y, cn.y);
+      return make_float2((float)nx, (float)ny);
+    }
+    return make_float2((float)cn.x, (float)cn.y);
+  }
+};
+
+// ADMM: state z, v (complex64).  u = z - v is the operator input;
+// c = a*u + g (+extra) ; z' = S_kappa(c + v) ; v' = v + (c - z') ; u' = z' - v'.
+// reference: pkg/src/bccblasso/solvers.py:385-448 (loop 426-436).
+struct EpiAdmm {
+  float2* z;
+  float2* v;
+  float2* c_out;                   // optional: c of this iteration (last iteration only)
+  const float2* __restrict__ extra;
+  const double* __restrict__ tau;
+  int* first_bad;
+  double a, kscale, extra_scale;
+  int it;
+  __device__ __forceinline__ float2 load(long long pos, int) const {
+    const float2 zz = z[pos], vv = v[pos];
+    return make_float2(zz.x - vv.x, zz.y - vv.y);
+  }
+  __device__ __forceinline__ float2 step(float2 zz, float2 vv, float2 g, float2 e, int b,
+                                         float2& zn, float2& vn, float2& cc) const {
+    const double ur = (double)zz.x - (double)vv.x, ui = (double)zz.y - (double)vv.y;
+    double cr = __fma_rn(a, ur, (double)g.x);
+    double ci = __fma_rn(a, ui, (double)g.y);
+    if (extra) {
+      cr = __fma_rn(extra_scale, (double)e.x, cr);
+      ci = __fma_rn(extra_scale, (double)e.y, ci);
+    }
+    if (!isfinite(cr) || !isfinite(ci)) atomicMin(first_bad + b, it);
+    const double sr = cr + (double)vv.x, si = ci + (double)vv.y;
+    const double kap = kscale * tau[b];
+    const double m2 = sr * sr + si * si;
+    double nzr, nzi;
+    if (m2 <= kap * kap) {
+      nzr = 0.0;
+      nzi = 0.0;
+    } else {
+      const double f = 1.0 - kap / sqrt(m2);
+      nzr = sr * f;
+      nzi = si * f;
+    }
+    const double nvr = (double)vv.x + (cr - nzr), nvi = (double)vv.y + (ci - nzi);
+    zn = make_float2((float)nzr, (float)nzi);
+    vn = make_float2((float)nvr, (float)nvi);
+    cc = make_float2((float)cr, (float)ci);
+    return make_float2(zn.x - vn.x, zn.y - vn.y);
+  }
+};
+
+// ------------------------------------------------------------------ pass A
+struct RowsIO {
+  const float2* __restrict__ V;  // [B][K1][L2]  (inverse input)
+  float2* __restrict__ U;        // [B][K1][L2]  (forward output)
+};
+
+template <int KP>
+__device__ __forceinline__ void rows_load_band(const Geo& G, const Axis& ax, const RowsIO& io,
+                                               float2* Xs, long long row0) {
+  const int K = ax.K, TR = G.TR, XP = K + 1;
+  for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
+    const int k = idx / TR, ii = idx - k * TR;
+    const long long gr = row0 + ii;
+    if (gr < G.rows) {
+      const long long b = gr / G.L2, l2 = gr - b * G.L2;
+      Xs[ii * XP + k] = io.V[(b * K + k) * G.L2 + l2];
+    }
+  }
+}
+
+template <int KP>
+__device__ __forceinline__ void rows_forward_store(const Geo& G, const Axis& ax, const RowsIO& io,
+                                                   float2 (&a)[KP], bool active, int ii_self, int s,
+                                                   float2* Xs, float2* S, long long row0) {
+  const int K = ax.K, TR = G.TR, XP = K + 1;
+  const int SP = KP * ax.pitch;  // per-line transpose buffer size
+  if (active) {
+    reg_dft<KP, false>(a);
+    band_fwd_scatter<KP>(a, s, ax, S + ii_self * SP);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
+    const int ii = idx / K, o = idx - ii * K;
+    if (row0 + ii < G.rows) Xs[ii * XP + o] = band_fwd_output(S + ii * SP, o, KP, ax);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
+    const int k = idx / TR, ii = idx - k * TR;
+    const long long gr = row0 + ii;
+    if (gr < G.rows) {
+      const long long b = gr / G.L2, l2 = gr - b * G.L2;
+      io.U[(b * K + k) * G.L2 + l2] = Xs[ii * XP + k];
+    }
+  }
+}
+
+// Generic pass A for plain-vector epilogues.
+template <int KP>
+__global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, Axis ax, RowsIO io, EpiVector epi) {
+  extern __shared__ float2 smem[];
+  const int R = ax.R, K = ax.K;
+  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
+  const long long row0 = (long long)blockIdx.x * G.TR;
+  const long long gr = row0 + ii;
+  const bool active = (ii < G.TR) && (gr < G.rows);
+  float2* Xs = smem;
+  float2* S = smem + G.TR * (K + 1);
+  float2 a[KP];
+  if (G.do_inv) {
+    rows_load_band<KP>(G, ax, io, Xs, row0);
+    __syncthreads();
+    if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
+  }
+  if (active) {
+    const long long base = gr * G.L1 + s;
+    const int b = (int)(gr / G.L2);
+    float mx = 0.f;
+#pragma unroll
+    for (int r = 0; r < KP; ++r) {
+      const long long pos = base + (long long)R * r;
+      a[r] = G.do_inv ? epi.update(pos, b, a[r]) : epi.load(pos, b);
+      mx = fmaxf(mx, sqrtf(a[r].x * a[r].x + a[r].y * a[r].y));
+    }
+    if (G.do_inv && epi.maxabs) group_atomic_max(epi.maxabs, b, mx);
+  }
+  if (G.do_fwd) {
+    if (G.do_inv) __syncthreads();  // Xs reuse
+    rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
+  }
+}
+
+// Pass A for ISTA / FISTA with a software-pipelined state stream (loads of the
+// next chunk are issued before the stores of the current one; state is in place).
+template <int KP, int CH>
+__global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, Axis ax, RowsIO io, EpiFista epi) {
+  extern __shared__ float2 smem[];
+  const int R = ax.R, K = ax.K;
+  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
+  const long long row0 = (long long)blockIdx.x * G.TR;
+  const long long gr = row0 + ii;
+  const bool active = (ii < G.TR) && (gr < G.rows);
+  float2* Xs = smem;
+  float2* S = smem + G.TR * (K + 1);
+  float2 a[KP];
+  if (G.do_inv) {
+    rows_load_band<KP>(G, ax, io, Xs, row0);
+    __syncthreads();
+    if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
+  }
+  if (active) {
+    const long long base = gr * G.L1 + s;
+    const int b = (int)(gr / G.L2);
+    if (!G.do_inv) {
+#pragma unroll
+      for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
+    } else {
+      double2 cb[CH];
+      float2 db[CH], eb[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const long long pos = base + (long long)R * q;
+        cb[q] = epi.c[pos];
+        db[q] = epi.momentum ? epi.d[pos] : make_float2(0.f, 0.f);
+        eb[q] = epi.extra ? epi.extra[pos] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int r0 = 0; r0 < KP; r0 += CH) {
+        double2 cn[CH];
+        float2 dn[CH], en[CH];
+        if (r0 + CH < KP) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const long long pos = base + (long long)R * (r0 + CH + q);
+            cn[q] = epi.c[pos];
+            dn[q] = epi.momentum ? epi.d[pos] : make_float2(0.f, 0.f);
+            en[q] = epi.extra ? epi.extra[pos] : make_float2(0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const long long pos = base + (long long)R * (r0 + q);
+          double2 cnew;
+          float2 dnew;
+          a[r0 + q] = epi.step(cb[q], db[q], a[r0 + q], eb[q], b, cnew, dnew);
+          epi.c[pos] = cnew;
+          if (epi.momentum) epi.d[pos] = dnew;
+        }
+        if (r0 + CH < KP) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            cb[q] = cn[q];
+            db[q] = dn[q];
+            eb[q] = en[q];
+          }
+        }
+      }
+    }
+  }
+  if (G.do_fwd) {
+    if (G.do_inv) __syncthreads();
+    rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
+  }
+}
+
+template <int KP, int CH>
+__global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, Axis ax, RowsIO io, EpiAdmm epi) {
+  extern __shared__ float2 smem[];
+  const int R = ax.R, K = ax.K;
+  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
+  const long long row0 = (long long)blockIdx.x * G.TR;
+  const long long gr = row0 + ii;
+  const bool active = (ii < G.TR) && (gr < G.rows);
+  float2* Xs = smem;
+  float2* S = smem + G.TR * (K + 1);
+  float2 a[KP];
+  if (G.do_inv) {
+    rows_load_band<KP>(G, ax, io, Xs, row0);
+    __syncthreads();
+    if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
+  }
+  if (active) {
+    const long long base = gr * G.L1 + s;
+    const int b = (int)(gr / G.L2);
+    if (!G.do_inv) {
+#pragma unroll
+      for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
+    } else {
+      float2 zb[CH], vb[CH], eb[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const long long pos = base + (long long)R * q;
+        zb[q] = epi.z[pos];
+        vb[q] = epi.v[pos];
+        eb[q] = epi.extra ? epi.extra[pos] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int r0 = 0; r0 < KP; r0 += CH) {
+        float2 zn[CH], vn[CH], en[CH];
+        if (r0 + CH < KP) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const long long pos = base + (long long)R * (r0 + CH + q);
+            zn[q] = epi.z[pos];
+            vn[q] = epi.v[pos];
+            en[q] = epi.extra ? epi.extra[pos] : make_float2(0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const long long pos = base + (long long)R * (r0 + q);
+          float2 znew, vnew, cc;
+          a[r0 + q] = epi.step(zb[q], vb[q], a[r0 + q], eb[q], b, znew, vnew, cc);
+          epi.z[pos] = znew;
+          epi.v[pos] = vnew;
+          if (epi.c_out) epi.c_out[pos] = cc;
+        }
+        if (r0 + CH < KP) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            zb[q] = zn[q];
+            vb[q] = vn[q];
+            eb[q] = en[q];
+          }
+        }
+      }
+    }
+  }
+  if (G.do_fwd) {
+    if (G.do_inv) __syncthreads();
+    rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
+  }
+}
+
+// ------------------------------------------------------------------ pass B
+struct ColsIO {
+  const float2* __restrict__ U;     // [B][K1][L2] forward input (do_fwd)
+  float2* __restrict__ V;           // [B][K1][L2] inverse output (do_inv)
+  const float2* __restrict__ D;     // [K1][K2] multiplier (null => identity)
+  const float2* __restrict__ P;     // [K1][K2] rhs multiplier (null => 1)
+  const float2* __restrict__ Bh;    // [B][K1][K2] rhs box (null => none)
+  float2* __restrict__ box_out;     // [B][K1][K2] (used when !do_inv)
+  int K1;
+};
+
+// One line = (snapshot b, column k1): length L2, band K2.
+template <int KP>
+__global__ void __launch_bounds__(256) cols_kernel(Geo G, Axis ax, ColsIO io) {
+  extern __shared__ float2 smem[];
+  const int R = ax.R, K = ax.K, N = ax.N;
+  const int TR = G.TR, XP = K + 1, SP = KP * ax.pitch;
+  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
+  const long long row0 = (long long)blockIdx.x * TR;
+  const long long gr = row0 + ii;
+  const bool active = (ii < TR) && (gr < G.rows);
+  float2* Xs = smem;
+  float2* S = smem + TR * XP;
+  float2 a[KP];
+  if (G.do_fwd) {
+    if (active) {
+      const float2* line = io.U + gr * N + s;
+#pragma unroll
+      for (int r = 0; r < KP; ++r) a[r] = line[(long long)R * r];
+      reg_dft<KP, false>(a);
+      band_fwd_scatter<KP>(a, s, ax, S + ii * SP);
+    }
+    __syncthreads();
+  }
+  // band values: Y = D*X + P*Bh
+  for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
+    const int i2 = idx / K, o = idx - i2 * K;
+    const long long g2 = row0 + i2;
+    if (g2 >= G.rows) continue;
+    const long long k1 = g2 % io.K1;
+    float2 y = make_float2(0.f, 0.f);
+    if (G.do_fwd) {
+      y = band_fwd_output(S + i2 * SP, o, KP, ax);
+      if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
+    }
+    if (io.Bh) {
+      float2 bh = io.Bh[g2 * K + o];
+      if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
+      y = cadd(y, bh);
+    }
+    Xs[i2 * XP + o] = y;
+  }
+  __syncthreads();
+  if (G.do_inv) {
+    if (active) {
+      band_inverse<KP>(Xs + ii * XP, s, ax, a);
+      float2* line = io.V + gr * N + s;
+#pragma unroll
+      for (int r = 0; r < KP; ++r) line[(long long)R * r] = a[r];
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
+      const int i2 = idx / K, o = idx - i2 * K;
+      const long long g2 = row0 + i2;
+      if (g2 < G.rows) io.box_out[g2 * K + o] = Xs[i2 * XP + o];
+    }
+  }
+}
+
+}  // namespace bccb
