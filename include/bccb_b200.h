@@ -83,6 +83,10 @@ size_t bccb_workspace_bytes(bccb_plan_t plan, int batch);
 int bccb_matvec(bccb_plan_t plan, int batch, const void* x, void* y, void* workspace,
                 void* stream);
 
+/* Same in complex128 end to end (complex128 band FFTs): drop-in precision for float64 callers. */
+int bccb_matvec_z(bccb_plan_t plan, int batch, const void* x, void* y, void* workspace,
+                  void* stream);
+
 /* out_box = fft2(x) restricted to the box (complex64 [batch][K1][K2]).
  * Replaces the spectrum computation np.fft.fft2 of bccb.py:104/123 for a band. */
 int bccb_spectrum_box(bccb_plan_t plan, int batch, const void* x, void* out_box, void* workspace,
@@ -129,8 +133,11 @@ int bccb_fista_run(bccb_plan_t plan, int batch, int first_iteration, int iterati
  * Replaces admm_solve (solvers.py:385-448): precompute P = (G + rho I)^-1, q = P b
  * (403-415) folded into the spectral box; loop c = q + rho P(z - v), z = S_{rho tau}(c + v),
  * v = v + (c - z) (426-436).
- *   z, v     : device complex64 [batch][L2][L1] (in: initial z / zeros; out: final)
- *   c_last   : device complex64 [batch][L2][L1] <- c of the last iteration (may be NULL)
+ *   z        : device complex64  [batch][L2][L1] (in: initial z; out: final z = the estimate)
+ *   v        : device complex128 [batch][L2][L1] scaled dual (in: zeros; out: final)
+ *   c_last   : device complex128 [batch][L2][L1] <- c of the last iteration (may be NULL)
+ * Runs on the complex128 band engine: v grows like t*|q| when z stays 0 (config 3, SURVEY
+ * finding 7) and the band correction cancels it, so complex64 would lose ~log2(t) bits.
  * Returns BCCB_ERR_SINGULAR if G + rho I is numerically singular (bccb.py:133-148). */
 int bccb_admm_run(bccb_plan_t plan, int batch, int first_iteration, int iterations, double rho,
                   const double* tau,
@@ -149,6 +156,18 @@ size_t bccb_topk_workspace_bytes(int batch, long long length, int k);
  *   mag : device float [batch][k] |values| at those indices (may be NULL) */
 int bccb_topk(int batch, long long length, const void* values, int is_double, int k, int* idx,
               float* mag, void* workspace, void* stream);
+
+/* ---------------------------------------------------------------- accounting */
+
+/* Total kernel launches issued by the library in this process (bench: gpu_launches). */
+long long bccb_launch_count(void);
+
+/* Bracket every launch of this thread with CUDA events on its stream until
+ * bccb_profile_end, which synchronises and returns the summed device time and launch
+ * count per kernel kind: [0] rows pass (band IFFT + solver epilogue + band FFT),
+ * [1] column pass (band FFT * spectrum + band IFFT), [2] other (setup, scatter). */
+int bccb_profile_begin(void);
+int bccb_profile_end(double* ms_by_kind, long long* launches_by_kind);
 
 #ifdef __cplusplus
 }

@@ -1,6 +1,7 @@
 """Build the sm_100a shared library in-tree (no JIT cache: the .so travels with the repo).
 
-`python -m paper_2509_13592_b200._build` or `__graft_entry__.build()`.
+`python paper_2509_13592_b200/_build.py` or `__graft_entry__.build()` (run as a file:
+importing the package first would load the previous library).
 """
 
 import os

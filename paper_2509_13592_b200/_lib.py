@@ -38,6 +38,7 @@ SIGNATURES = {
     "bccb_plan_eigen_box": (_i, [_vp, _vp, ctypes.POINTER(_d), ctypes.POINTER(_d)]),
     "bccb_workspace_bytes": (_sz, [_vp, _i]),
     "bccb_matvec": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "bccb_matvec_z": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "bccb_spectrum_box": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "bccb_synthesize": (_i, [_vp, _i, _vp, _f, _vp, _f, _vp, _vp, _vp, _vp]),
     "bccb_adjoint": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -45,13 +46,16 @@ SIGNATURES = {
     "bccb_admm_run": (_i, [_vp, _i, _i, _i, _d] + [_vp] * 9),
     "bccb_topk_workspace_bytes": (_sz, [_i, _ll, _i]),
     "bccb_topk": (_i, [_i, _ll, _vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "bccb_launch_count": (_ll, []),
+    "bccb_profile_begin": (_i, []),
+    "bccb_profile_end": (_i, [_vp, _vp]),
 }
 
 
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2509_13592_b200._build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2509_13592_b200/_build.py` "
             "(there is no CPU fallback for the BCCB GPU path)"
         )
     lib = ctypes.CDLL(LIB_PATH)

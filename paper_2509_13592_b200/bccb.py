@@ -262,18 +262,25 @@ def _batched_view(c, dim: int, l2: int = 0, l1: int = 0):
 def bccb_matvec(op: BccbOperator, c):
     """Apply the operator: band FFT, eigenvalue multiply, band IFFT (bccb.py:113-125).
 
-    c: (L,) / (B, L) / (B, L2, L1), numpy or CUDA tensor.  Numpy in -> complex128
-    numpy out (computed in complex64 on the GPU); tensor in -> complex64 tensor out.
+    c: (L,) / (B, L) / (B, L2, L1), numpy or CUDA tensor.  float64 inputs (numpy, or
+    complex128 tensors) run the complex128 band engine and return complex128; complex64
+    tensors run the complex64 engine.
     """
     t, batch, was_numpy, batch_shape = _batched_view(c, op.dimension, op.l2, op.l1)
-    x = _as_device_c64(t, op.device).reshape(batch, op.dimension)
+    wide = was_numpy or t.dtype in (torch.complex128, torch.float64)
+    dtype = torch.complex128 if wide else torch.complex64
+    if isinstance(t, torch.Tensor):
+        x = t.to(device=f"cuda:{op.device}", dtype=dtype).contiguous()
+    else:
+        x = torch.from_numpy(np.ascontiguousarray(t, dtype=np.complex128)).to(f"cuda:{op.device}")
+    x = x.reshape(batch, op.dimension)
     y = torch.empty_like(x)
-    _lib.check(_lib.lib.bccb_matvec(op._plan, batch, x.data_ptr(), y.data_ptr(),
-                                    op.workspace(batch).data_ptr(), _stream_ptr(op.device)))
-    out_shape = tuple(t.shape)
-    y = y.reshape(out_shape)
+    fn = _lib.lib.bccb_matvec_z if wide else _lib.lib.bccb_matvec
+    _lib.check(fn(op._plan, batch, x.data_ptr(), y.data_ptr(), op.workspace(batch).data_ptr(),
+                  _stream_ptr(op.device)))
+    y = y.reshape(tuple(t.shape))
     if was_numpy:
-        return y.cpu().numpy().astype(np.complex128)
+        return y.cpu().numpy()
     return y
 
 

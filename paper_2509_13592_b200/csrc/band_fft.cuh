@@ -14,19 +14,24 @@
 // R-term reduction (forward) or broadcast (inverse) through shared memory.
 // With K << N (K1/L1 = 1/32 at config 5) this is far cheaper than a full FFT
 // and keeps every HBM access 128-bit / coalesced (lanes own consecutive s).
+//
+// The engine is generic over the complex type: float2 (FISTA / ISTA / matvec) or
+// double2 (ADMM, whose dual grows like t*|q| in the degenerate config-3 regime and
+// cancels against the band correction — see DESIGN.md "precision").
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace bccb {
 
-constexpr int KP_MAX = 32;
+constexpr int KP_MAX = 32;     // register DFT size cap, complex64
+constexpr int KP_MAX_D = 16;   // register DFT size cap, complex128
 
-// Forward 64th roots of unity: c_roots64[t] = exp(-2 pi i t / 64).  Filled once
-// per device by the host (plan creation); indexed with compile-time constants so
-// every access becomes a constant-bank operand of the FFMA.  (Single translation
-// unit: the library is built from bccb_capi.cu alone, no -rdc needed.)
+// Forward 64th roots of unity exp(-2 pi i t / 64).  Filled once per device by the host;
+// indexed with compile-time constants so each access is a constant-bank operand.
+// (Single translation unit: the library is built from bccb_capi.cu alone, no -rdc.)
 __constant__ float2 c_roots64[64];
+__constant__ double2 c_roots64d[64];
 
 template <int P> struct Log2 { static constexpr int v = Log2<P / 2>::v + 1; };
 template <> struct Log2<1> { static constexpr int v = 0; };
@@ -37,13 +42,25 @@ __host__ __device__ constexpr int bit_reverse(int x, int bits) {
   return r;
 }
 
+// ---- complex helpers (float2 / double2 overloads)
+__device__ __forceinline__ float2 cmake(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ double2 cmake(double a, double b) { return make_double2(a, b); }
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 // a * conj(b)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
 }
 // acc += a * b
 __device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
@@ -53,17 +70,32 @@ __device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
   acc.y = fmaf(a.y, b.x, acc.y);
   return acc;
 }
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ float2 to_c(float2 v, float2) { return v; }
+__device__ __forceinline__ double2 to_c(float2 v, double2) { return make_double2(v.x, v.y); }
+__device__ __forceinline__ double2 to_c(double2 v, double2) { return v; }
+__device__ __forceinline__ float2 to_c(double2 v, float2) { return make_float2((float)v.x, (float)v.y); }
+
+template <typename C> __device__ __forceinline__ C root64(int t);
+template <> __device__ __forceinline__ float2 root64<float2>(int t) { return c_roots64[t]; }
+template <> __device__ __forceinline__ double2 root64<double2>(int t) { return c_roots64d[t]; }
 
 // In-register radix-2 DIT DFT of size P (P divides 64), natural order in/out.
 // INV=false: A[j] = sum_r a[r] e^{-2 pi i r j / P};  INV=true: e^{+...} (unnormalised).
-template <int P, bool INV>
-__device__ __forceinline__ void reg_dft(float2 (&a)[P]) {
+template <int P, bool INV, typename C>
+__device__ __forceinline__ void reg_dft(C (&a)[P]) {
   constexpr int LG = Log2<P>::v;
 #pragma unroll
   for (int i = 0; i < P; ++i) {
     const int j = bit_reverse(i, LG);
     if (j > i) {
-      const float2 t = a[i];
+      const C t = a[i];
       a[i] = a[j];
       a[j] = t;
     }
@@ -75,54 +107,55 @@ __device__ __forceinline__ void reg_dft(float2 (&a)[P]) {
       const int t = k * (64 / (2 * half));
 #pragma unroll
       for (int i = 0; i < P; i += 2 * half) {
-        const float2 u = a[i + k];
-        float2 v = a[i + k + half];
+        const C u = a[i + k];
+        C v = a[i + k + half];
         if (t == 16) {
           // w = -i (forward) / +i (inverse)
-          v = INV ? make_float2(-v.y, v.x) : make_float2(v.y, -v.x);
+          v = INV ? cmake(-v.y, v.x) : cmake(v.y, -v.x);
         } else if (t != 0) {
-          float2 w = c_roots64[t];
+          C w = root64<C>(t);
           if (INV) w.y = -w.y;
           v = cmul(v, w);
         }
-        a[i + k] = make_float2(u.x + v.x, u.y + v.y);
-        a[i + k + half] = make_float2(u.x - v.x, u.y - v.y);
+        a[i + k] = cadd(u, v);
+        a[i + k + half] = csub(u, v);
       }
     }
   }
 }
 
-// Runtime geometry of one axis (built on the host, see bccb_capi.cu: make_axis).
-struct Axis {
+// Runtime geometry of one axis at one precision (built on the host: make_axis).
+template <typename C>
+struct AxisT {
   int N;      // line length (L1 for rows, L2 for columns)
   int K;      // band (multiple of KP, <= N)
   int KP;     // register DFT size (compile-time copy in the kernels)
   int R;      // N / KP: threads per line team
   int Mo;     // K / KP
   int pitch;  // shared-memory row pitch for the level-2 transpose (odd)
-  const float2* tw1;  // [KP][R]  w_N^{s j}
-  const float2* tw2;  // [Mo][R]  w_R^{s m}
+  const C* tw1;  // [KP][R]  w_N^{s j}
+  const C* tw2;  // [Mo][R]  w_R^{s m}
 };
 
 // Level-2 forward, part 1: thread s scatters T[j] = A[j] * w_N^{s j} into the
-// line's transpose buffer S[j][s] (pitch = axis.pitch, odd => conflict-free reads).
-template <int KP>
-__device__ __forceinline__ void band_fwd_scatter(const float2 (&A)[KP], int s, const Axis& ax,
-                                                 float2* __restrict__ S) {
+// line's transpose buffer S[j][s] (odd pitch => conflict-free reads in part 2).
+template <int KP, typename C>
+__device__ __forceinline__ void band_fwd_scatter(const C (&A)[KP], int s, const AxisT<C>& ax,
+                                                 C* __restrict__ S) {
 #pragma unroll
   for (int j = 0; j < KP; ++j) {
-    const float2 w = __ldg(ax.tw1 + j * ax.R + s);
+    const C w = __ldg(ax.tw1 + j * ax.R + s);
     S[j * ax.pitch + s] = cmul(A[j], w);
   }
 }
 
 // Level-2 forward, part 2: band output o = j + KP*m of a line from its S buffer.
-__device__ __forceinline__ float2 band_fwd_output(const float2* __restrict__ S, int o, int KP,
-                                                  const Axis& ax) {
+template <typename C>
+__device__ __forceinline__ C band_fwd_output(const C* __restrict__ S, int o, int KP, const AxisT<C>& ax) {
   const int j = o % KP;
   const int m = o / KP;
-  const float2* row = S + j * ax.pitch;
-  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+  const C* row = S + j * ax.pitch;
+  C acc0 = cmake(decltype(C::x)(0), decltype(C::x)(0)), acc1 = acc0;
   const int R = ax.R;
   if (m == 0) {
     int s = 0;
@@ -133,7 +166,7 @@ __device__ __forceinline__ float2 band_fwd_output(const float2* __restrict__ S, 
     }
     if (s < R) acc0 = cadd(acc0, row[s]);
   } else {
-    const float2* tw = ax.tw2 + m * R;
+    const C* tw = ax.tw2 + m * R;
     int s = 0;
 #pragma unroll 4
     for (; s + 1 < R; s += 2) {
@@ -148,9 +181,9 @@ __device__ __forceinline__ float2 band_fwd_output(const float2* __restrict__ S, 
 // Level-2 inverse + level-1 inverse DFT: thread s of a line team turns the K band
 // values Y (shared memory, one line) into its KP outputs g[r] = x[R*r + s]
 // (unnormalised inverse).
-template <int KP>
-__device__ __forceinline__ void band_inverse(const float2* __restrict__ Y, int s, const Axis& ax,
-                                             float2 (&g)[KP]) {
+template <int KP, typename C>
+__device__ __forceinline__ void band_inverse(const C* __restrict__ Y, int s, const AxisT<C>& ax,
+                                             C (&g)[KP]) {
   if (ax.Mo == 1) {
 #pragma unroll
     for (int j = 0; j < KP; ++j) g[j] = cmulc(Y[j], __ldg(ax.tw1 + j * ax.R + s));
@@ -158,12 +191,9 @@ __device__ __forceinline__ void band_inverse(const float2* __restrict__ Y, int s
 #pragma unroll
     for (int j = 0; j < KP; ++j) g[j] = Y[j];
     for (int m = 1; m < ax.Mo; ++m) {
-      const float2 w2 = __ldg(ax.tw2 + m * ax.R + s);
+      const C w2 = __ldg(ax.tw2 + m * ax.R + s);
 #pragma unroll
-      for (int j = 0; j < KP; ++j) {
-        const float2 t = cmulc(Y[j + KP * m], w2);
-        g[j] = cadd(g[j], t);
-      }
+      for (int j = 0; j < KP; ++j) g[j] = cadd(g[j], cmulc(Y[j + KP * m], w2));
     }
 #pragma unroll
     for (int j = 0; j < KP; ++j) g[j] = cmulc(g[j], __ldg(ax.tw1 + j * ax.R + s));

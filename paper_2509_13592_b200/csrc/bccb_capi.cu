@@ -9,8 +9,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/bccb_b200.h"
@@ -49,6 +51,65 @@ static int fail(int code, const char* fmt, ...) {
   } while (0)
 
 extern "C" const char* bccb_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------ launch accounting
+// Every kernel launch is counted (bccb_launch_count); between bccb_profile_begin/end each
+// launch is also bracketed by CUDA events on its own stream, grouped by kernel kind.
+enum KernelKind { KIND_ROWS = 0, KIND_COLS = 1, KIND_OTHER = 2, KIND_COUNT = 3 };
+static std::atomic<long long> g_launches{0};
+struct ProfEvent {
+  cudaEvent_t a, b;
+  int kind;
+};
+static thread_local bool g_prof_on = false;
+static thread_local std::vector<ProfEvent> g_prof_events;
+static thread_local size_t g_prof_used = 0;
+
+static void prof_before(int kind, cudaStream_t st, ProfEvent** slot) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  *slot = nullptr;
+  if (!g_prof_on) return;
+  if (g_prof_used == g_prof_events.size()) {
+    ProfEvent e;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    g_prof_events.push_back(e);
+  }
+  ProfEvent* e = &g_prof_events[g_prof_used++];
+  e->kind = kind;
+  cudaEventRecord(e->a, st);
+  *slot = e;
+}
+static void prof_after(ProfEvent* e, cudaStream_t st) {
+  if (e) cudaEventRecord(e->b, st);
+}
+
+extern "C" long long bccb_launch_count(void) { return g_launches.load(); }
+
+extern "C" int bccb_profile_begin(void) {
+  g_prof_on = true;
+  g_prof_used = 0;
+  return BCCB_OK;
+}
+
+extern "C" int bccb_profile_end(double* ms_by_kind, long long* launches_by_kind) {
+  g_prof_on = false;
+  for (int k = 0; k < KIND_COUNT; ++k) {
+    if (ms_by_kind) ms_by_kind[k] = 0.0;
+    if (launches_by_kind) launches_by_kind[k] = 0;
+  }
+  for (size_t i = 0; i < g_prof_used; ++i) {
+    ProfEvent& e = g_prof_events[i];
+    cudaError_t err = cudaEventSynchronize(e.b);
+    if (err != cudaSuccess) return fail(BCCB_ERR_CUDA, "profile sync: %s", cudaGetErrorString(err));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    if (ms_by_kind) ms_by_kind[e.kind] += ms;
+    if (launches_by_kind) launches_by_kind[e.kind] += 1;
+  }
+  g_prof_used = 0;
+  return BCCB_OK;
+}
 extern "C" const char* bccb_version(void) { return "bccb_b200 0.1.0 (sm_100a)"; }
 
 // ------------------------------------------------------------------ device init
@@ -60,33 +121,48 @@ static int ensure_device_constants(int device) {
   if (device < 0 || device >= 64) return fail(BCCB_ERR_INVALID, "bad device %d", device);
   if (g_roots_ready[device]) return BCCB_OK;
   float2 roots[64];
+  double2 rootsd[64];
   for (int t = 0; t < 64; ++t) {
     const double ang = -2.0 * M_PI * t / 64.0;
     roots[t] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    rootsd[t] = make_double2(std::cos(ang), std::sin(ang));
   }
   CUDA_TRY(cudaMemcpyToSymbol(c_roots64, roots, sizeof(roots)));
+  CUDA_TRY(cudaMemcpyToSymbol(c_roots64d, rootsd, sizeof(rootsd)));
   g_roots_ready[device] = true;
   return BCCB_OK;
 }
 
 // ------------------------------------------------------------------ plan
+// One axis at one precision (register DFT size, band, team size, twiddles).
+struct AxisPrec {
+  int KP = 1, R = 1, Mo = 1, pitch = 1;
+  void* tw1 = nullptr;  // [KP][R]  w_N^{s j}   (float2 or double2)
+  void* tw2 = nullptr;  // [Mo][R]  w_R^{s m}
+};
+
 struct AxisHost {
-  int N = 0, K = 0, KP = 1, R = 1, Mo = 1, pitch = 1;
-  float2* tw1 = nullptr;
-  float2* tw2 = nullptr;
-  Axis dev() const {
-    Axis a;
+  int N = 0, K = 0;
+  AxisPrec f, d;  // complex64 engine (KP <= 32), complex128 engine (KP <= 16)
+  template <typename C>
+  const AxisPrec& prec() const;
+  template <typename C>
+  AxisT<C> dev() const {
+    const AxisPrec& p = prec<C>();
+    AxisT<C> a;
     a.N = N;
     a.K = K;
-    a.KP = KP;
-    a.R = R;
-    a.Mo = Mo;
-    a.pitch = pitch;
-    a.tw1 = tw1;
-    a.tw2 = tw2;
+    a.KP = p.KP;
+    a.R = p.R;
+    a.Mo = p.Mo;
+    a.pitch = p.pitch;
+    a.tw1 = (const C*)p.tw1;
+    a.tw2 = (const C*)p.tw2;
     return a;
   }
 };
+template <> const AxisPrec& AxisHost::prec<float2>() const { return f; }
+template <> const AxisPrec& AxisHost::prec<double2>() const { return d; }
 
 struct bccb_plan_s {
   int device = 0;
@@ -101,19 +177,37 @@ struct bccb_plan_s {
   bool full() const { return ax1.K == L1 && ax2.K == L2; }
 };
 
-static int pow2_floor(int x) {
-  int p = 1;
-  while (p * 2 <= x) p *= 2;
-  return p;
-}
 static int pow2_ceil(int x) {
   int p = 1;
   while (p < x) p *= 2;
   return p;
 }
 
+template <typename C>
+static int upload_twiddles(int N, AxisPrec& ap) {
+  std::vector<C> t1((size_t)ap.KP * ap.R), t2((size_t)ap.Mo * ap.R);
+  for (int j = 0; j < ap.KP; ++j)
+    for (int s = 0; s < ap.R; ++s) {
+      // w_N^{s j}; the exponent is reduced mod N in integers for accuracy
+      const long long e = ((long long)s * j) % N;
+      const double ang = -2.0 * M_PI * (double)e / (double)N;
+      t1[(size_t)j * ap.R + s] = C{(decltype(C::x))std::cos(ang), (decltype(C::x))std::sin(ang)};
+    }
+  for (int m = 0; m < ap.Mo; ++m)
+    for (int s = 0; s < ap.R; ++s) {
+      const long long e = ((long long)s * m) % ap.R;
+      const double ang = -2.0 * M_PI * (double)e / (double)ap.R;
+      t2[(size_t)m * ap.R + s] = C{(decltype(C::x))std::cos(ang), (decltype(C::x))std::sin(ang)};
+    }
+  CUDA_TRY(cudaMalloc(&ap.tw1, t1.size() * sizeof(C)));
+  CUDA_TRY(cudaMalloc(&ap.tw2, t2.size() * sizeof(C)));
+  CUDA_TRY(cudaMemcpy(ap.tw1, t1.data(), t1.size() * sizeof(C), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(ap.tw2, t2.data(), t2.size() * sizeof(C), cudaMemcpyHostToDevice));
+  return BCCB_OK;
+}
+
 // Choose the register DFT size KP (largest power of two dividing N, <= 32 and <= the band),
-// round the band up to a multiple of KP and build the twiddle tables in double precision.
+// round the band up to a multiple of KP and build both precisions' twiddle tables.
 static int make_axis(int N, int Kreq, AxisHost& ax) {
   int KP = 1;
   while (KP < KP_MAX && N % (KP * 2) == 0) KP *= 2;
@@ -121,37 +215,32 @@ static int make_axis(int N, int Kreq, AxisHost& ax) {
   int K = ((Kreq + KP - 1) / KP) * KP;
   K = std::min(K, N);
   if (K % KP != 0) K = N;  // N is a multiple of KP
-  const int R = N / KP;
-  if (R > 1024)
-    return fail(BCCB_ERR_UNSUPPORTED,
-                "grid length %d needs %d threads per line (> 1024); use a length with a larger "
-                "power-of-two factor",
-                N, R);
   ax.N = N;
   ax.K = K;
-  ax.KP = KP;
-  ax.R = R;
-  ax.Mo = K / KP;
-  ax.pitch = (R % 2 == 1) ? R : R + 1;
-  std::vector<float2> t1((size_t)KP * R), t2((size_t)ax.Mo * R);
-  for (int j = 0; j < KP; ++j)
-    for (int s = 0; s < R; ++s) {
-      // w_N^{s j}; reduce the exponent mod N in integers for accuracy
-      const long long e = ((long long)s * j) % N;
-      const double ang = -2.0 * M_PI * (double)e / (double)N;
-      t1[(size_t)j * R + s] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-    }
-  for (int m = 0; m < ax.Mo; ++m)
-    for (int s = 0; s < R; ++s) {
-      const long long e = ((long long)s * m) % R;
-      const double ang = -2.0 * M_PI * (double)e / (double)R;
-      t2[(size_t)m * R + s] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-    }
-  CUDA_TRY(cudaMalloc(&ax.tw1, t1.size() * sizeof(float2)));
-  CUDA_TRY(cudaMalloc(&ax.tw2, t2.size() * sizeof(float2)));
-  CUDA_TRY(cudaMemcpy(ax.tw1, t1.data(), t1.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(ax.tw2, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  return BCCB_OK;
+  const int kps[2] = {KP, std::min(KP, KP_MAX_D)};
+  AxisPrec* aps[2] = {&ax.f, &ax.d};
+  for (int q = 0; q < 2; ++q) {
+    AxisPrec& ap = *aps[q];
+    ap.KP = kps[q];
+    ap.R = N / ap.KP;
+    if (ap.R > 1024)
+      return fail(BCCB_ERR_UNSUPPORTED,
+                  "grid length %d needs %d threads per line (> 1024); use a length with a larger "
+                  "power-of-two factor",
+                  N, ap.R);
+    ap.Mo = K / ap.KP;
+    ap.pitch = (ap.R % 2 == 1) ? ap.R : ap.R + 1;
+  }
+  int rc = upload_twiddles<float2>(N, ax.f);
+  if (!rc) rc = upload_twiddles<double2>(N, ax.d);
+  return rc;
+}
+
+static void free_axis(AxisHost& a) {
+  cudaFree(a.f.tw1);
+  cudaFree(a.f.tw2);
+  cudaFree(a.d.tw1);
+  cudaFree(a.d.tw2);
 }
 
 static void free_plan(bccb_plan_s* p) {
@@ -159,10 +248,8 @@ static void free_plan(bccb_plan_s* p) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(p->device);
-  cudaFree(p->ax1.tw1);
-  cudaFree(p->ax1.tw2);
-  cudaFree(p->ax2.tw1);
-  cudaFree(p->ax2.tw2);
+  free_axis(p->ax1);
+  free_axis(p->ax2);
   cudaFree(p->lam_box_dev);
   cudaFree(p->occ_dev);
   cudaSetDevice(cur);
@@ -323,33 +410,35 @@ extern "C" int bccb_plan_eigen_box(bccb_plan_t p, double* box_t, double* re, dou
 }
 
 // ------------------------------------------------------------------ workspace
+// U, V hold [batch][K1][L2] band intermediates and D, P the [K1][K2] multipliers; all are
+// sized for complex128 so one workspace serves both engines.
 struct Workspace {
-  float2* U;
-  float2* V;
-  float2* D;
-  float2* P;
+  void* U;
+  void* V;
+  void* D;
+  void* P;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static size_t ws_bytes(const bccb_plan_s* p, int batch) {
-  const size_t inter = (size_t)batch * p->ax1.K * p->L2 * sizeof(float2);
-  const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(float2);
+  const size_t inter = (size_t)batch * p->ax1.K * p->L2 * sizeof(double2);
+  const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
   return 2 * align_up(inter) + 2 * align_up(box);
 }
 
 static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   Workspace w;
   char* ptr = (char*)base;
-  const size_t inter = align_up((size_t)batch * p->ax1.K * p->L2 * sizeof(float2));
-  const size_t box = align_up((size_t)p->ax1.K * p->ax2.K * sizeof(float2));
-  w.U = (float2*)ptr;
+  const size_t inter = align_up((size_t)batch * p->ax1.K * p->L2 * sizeof(double2));
+  const size_t box = align_up((size_t)p->ax1.K * p->ax2.K * sizeof(double2));
+  w.U = ptr;
   ptr += inter;
-  w.V = (float2*)ptr;
+  w.V = ptr;
   ptr += inter;
-  w.D = (float2*)ptr;
+  w.D = ptr;
   ptr += box;
-  w.P = (float2*)ptr;
+  w.P = ptr;
   return w;
 }
 
@@ -364,11 +453,13 @@ struct LaunchShape {
   size_t smem;
 };
 
+template <typename C>
 static LaunchShape shape_for(const AxisHost& ax) {
+  const AxisPrec& ap = ax.prec<C>();
   LaunchShape s;
-  s.TR = std::max(1, 256 / ax.R);
-  s.threads = s.TR * ax.R;
-  s.smem = ((size_t)s.TR * (ax.K + 1) + (size_t)s.TR * ax.KP * ax.pitch) * sizeof(float2);
+  s.TR = std::max(1, 256 / ap.R);
+  s.threads = s.TR * ap.R;
+  s.smem = ((size_t)s.TR * (ax.K + 1) + (size_t)s.TR * ap.KP * ap.pitch) * sizeof(C);
   return s;
 }
 
@@ -381,15 +472,23 @@ static int prep_smem(KernelT kernel, size_t smem) {
   return BCCB_OK;
 }
 
-#define KP_DISPATCH(KPVAL, ...)            \
-  switch (KPVAL) {                          \
-    case 1: { constexpr int KPC = 1; __VA_ARGS__; } break;   \
-    case 2: { constexpr int KPC = 2; __VA_ARGS__; } break;   \
-    case 4: { constexpr int KPC = 4; __VA_ARGS__; } break;   \
-    case 8: { constexpr int KPC = 8; __VA_ARGS__; } break;   \
-    case 16: { constexpr int KPC = 16; __VA_ARGS__; } break; \
-    case 32: { constexpr int KPC = 32; __VA_ARGS__; } break; \
-    default: return fail(BCCB_ERR_UNSUPPORTED, "register DFT size %d", KPVAL); \
+// Register DFT size dispatch: complex64 engine up to 32, complex128 engine up to 16.
+#define KP_CASES_COMMON(...)                               \
+  case 1: { constexpr int KPC = 1; __VA_ARGS__; } break;   \
+  case 2: { constexpr int KPC = 2; __VA_ARGS__; } break;   \
+  case 4: { constexpr int KPC = 4; __VA_ARGS__; } break;   \
+  case 8: { constexpr int KPC = 8; __VA_ARGS__; } break;   \
+  case 16: { constexpr int KPC = 16; __VA_ARGS__; } break;
+#define KP_DISPATCH_F(KPVAL, ...)                                               \
+  switch (KPVAL) {                                                              \
+    KP_CASES_COMMON(__VA_ARGS__)                                                \
+    case 32: { constexpr int KPC = 32; __VA_ARGS__; } break;                    \
+    default: return fail(BCCB_ERR_UNSUPPORTED, "register DFT size %d", KPVAL);  \
+  }
+#define KP_DISPATCH_D(KPVAL, ...)                                               \
+  switch (KPVAL) {                                                              \
+    KP_CASES_COMMON(__VA_ARGS__)                                                \
+    default: return fail(BCCB_ERR_UNSUPPORTED, "register DFT size %d", KPVAL);  \
   }
 
 static Geo rows_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool inv, bool fwd) {
@@ -403,60 +502,67 @@ static Geo rows_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool
   return G;
 }
 
-static int launch_rows_vector(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
-                              const EpiVector& epi, cudaStream_t st) {
-  const LaunchShape sh = shape_for(p->ax1);
-  const Geo G = rows_geo(p, batch, sh, inv, fwd);
-  RowsIO io{w.V, w.U};
-  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  KP_DISPATCH(p->ax1.KP, {
-    auto k = rows_vector_kernel<KPC>;
-    int rc = prep_smem(k, sh.smem);
-    if (rc) return rc;
-    k<<<grid, sh.threads, sh.smem, st>>>(G, p->ax1.dev(), io, epi);
-  });
+template <typename C, typename KernelT, typename... Args>
+static int launch_pass(KernelT k, int kind, unsigned grid, const LaunchShape& sh, cudaStream_t st,
+                       Args... args) {
+  int rc = prep_smem(k, sh.smem);
+  if (rc) return rc;
+  ProfEvent* pe;
+  prof_before(kind, st, &pe);
+  k<<<grid, sh.threads, sh.smem, st>>>(args...);
+  prof_after(pe, st);
   LAUNCH_CHECK();
+  return BCCB_OK;
+}
+
+template <typename C>
+static int launch_rows_vector(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
+                              const EpiVector<C>& epi, cudaStream_t st) {
+  const LaunchShape sh = shape_for<C>(p->ax1);
+  const Geo G = rows_geo(p, batch, sh, inv, fwd);
+  RowsIO<C> io{(const C*)w.V, (C*)w.U};
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const AxisT<C> ax = p->ax1.dev<C>();
+  if constexpr (std::is_same<C, float2>::value) {
+    KP_DISPATCH_F(ax.KP, return launch_pass<C>(rows_vector_kernel<KPC, C>, KIND_ROWS, grid, sh, st, G, ax, io, epi));
+  } else {
+    KP_DISPATCH_D(ax.KP, return launch_pass<C>(rows_vector_kernel<KPC, C>, KIND_ROWS, grid, sh, st, G, ax, io, epi));
+  }
   return BCCB_OK;
 }
 
 static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                              const EpiFista& epi, cudaStream_t st) {
-  const LaunchShape sh = shape_for(p->ax1);
+  const LaunchShape sh = shape_for<float2>(p->ax1);
   const Geo G = rows_geo(p, batch, sh, inv, fwd);
-  RowsIO io{w.V, w.U};
+  RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  KP_DISPATCH(p->ax1.KP, {
+  const AxisT<float2> ax = p->ax1.dev<float2>();
+  KP_DISPATCH_F(ax.KP, {
     constexpr int CH = KPC < 4 ? KPC : 4;
-    auto k = rows_fista_kernel<KPC, CH>;
-    int rc = prep_smem(k, sh.smem);
-    if (rc) return rc;
-    k<<<grid, sh.threads, sh.smem, st>>>(G, p->ax1.dev(), io, epi);
+    return launch_pass<float2>(rows_fista_kernel<KPC, CH>, KIND_ROWS, grid, sh, st, G, ax, io, epi);
   });
-  LAUNCH_CHECK();
   return BCCB_OK;
 }
 
 static int launch_rows_admm(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                             const EpiAdmm& epi, cudaStream_t st) {
-  const LaunchShape sh = shape_for(p->ax1);
+  const LaunchShape sh = shape_for<double2>(p->ax1);
   const Geo G = rows_geo(p, batch, sh, inv, fwd);
-  RowsIO io{w.V, w.U};
+  RowsIO<double2> io{(const double2*)w.V, (double2*)w.U};
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  KP_DISPATCH(p->ax1.KP, {
+  const AxisT<double2> ax = p->ax1.dev<double2>();
+  KP_DISPATCH_D(ax.KP, {
     constexpr int CH = KPC < 4 ? KPC : 4;
-    auto k = rows_admm_kernel<KPC, CH>;
-    int rc = prep_smem(k, sh.smem);
-    if (rc) return rc;
-    k<<<grid, sh.threads, sh.smem, st>>>(G, p->ax1.dev(), io, epi);
+    return launch_pass<double2>(rows_admm_kernel<KPC, CH>, KIND_ROWS, grid, sh, st, G, ax, io, epi);
   });
-  LAUNCH_CHECK();
   return BCCB_OK;
 }
 
+template <typename C>
 static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, const Workspace& w,
-                       const float2* D, const float2* P, const float2* Bh, float2* box_out,
-                       cudaStream_t st) {
-  const LaunchShape sh = shape_for(p->ax2);
+                       const C* D, const C* P, const float2* Bh, C* box_out, cudaStream_t st) {
+  const LaunchShape sh = shape_for<C>(p->ax2);
   Geo G;
   G.L1 = p->L1;
   G.L2 = p->L2;
@@ -464,56 +570,61 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   G.TR = sh.TR;
   G.do_fwd = fwd ? 1 : 0;
   G.do_inv = inv ? 1 : 0;
-  ColsIO io;
-  io.U = w.U;
-  io.V = w.V;
+  ColsIO<C> io;
+  io.U = (const C*)w.U;
+  io.V = (C*)w.V;
   io.D = D;
   io.P = P;
   io.Bh = Bh;
   io.box_out = box_out;
   io.K1 = p->ax1.K;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  KP_DISPATCH(p->ax2.KP, {
-    auto k = cols_kernel<KPC>;
-    int rc = prep_smem(k, sh.smem);
-    if (rc) return rc;
-    k<<<grid, sh.threads, sh.smem, st>>>(G, p->ax2.dev(), io);
-  });
-  LAUNCH_CHECK();
+  const AxisT<C> ax = p->ax2.dev<C>();
+  if constexpr (std::is_same<C, float2>::value) {
+    KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
+  } else {
+    KP_DISPATCH_D(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
+  }
   return BCCB_OK;
 }
 
-// D / P boxes for one operation (complex64 [K1][K2]), from the complex128 eigenvalue box.
-//   mode 0 (matvec):  D = (lam - lam_out) / L,               P = -
+// D / P boxes for one operation ([K1][K2], complex64 or complex128), from the complex128
+// eigenvalue box (1/L of the unnormalised inverse folded in):
+//   mode 0 (matvec):  D = (lam - lam_out) / L
 //   mode 1 (ISTA):    D = -mu (lam - lam_out) / L,           P = mu / L
 //   mode 2 (ADMM):    D = (rho/(lam+rho) - a) / L,           P = 1 / ((lam + rho) L)
-//   mode 3 (synth):   D = -,                                  P = scale
+template <typename C>
 __global__ void coef_kernel(const double2* __restrict__ lam, int n, int mode, double s1,
-                            double lam_out, double a, double invL, float2* D, float2* P) {
+                            double lam_out, double a, double invL, C* D, C* P) {
+  using R = decltype(C::x);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double lr = lam[i].x, li = lam[i].y;
   if (mode == 0) {
-    D[i] = make_float2((float)((lr - lam_out) * invL), (float)(li * invL));
+    D[i] = C{(R)((lr - lam_out) * invL), (R)(li * invL)};
   } else if (mode == 1) {
-    D[i] = make_float2((float)(-s1 * (lr - lam_out) * invL), (float)(-s1 * li * invL));
-    P[i] = make_float2((float)(s1 * invL), 0.f);
+    D[i] = C{(R)(-s1 * (lr - lam_out) * invL), (R)(-s1 * li * invL)};
+    P[i] = C{(R)(s1 * invL), (R)0};
   } else if (mode == 2) {
     // q = 1/(lam + rho) ; D = rho*q - a
     const double dr = lr + s1, di = li;
     const double den = dr * dr + di * di;
     const double qr = dr / den, qi = -di / den;
-    D[i] = make_float2((float)((s1 * qr - a) * invL), (float)(s1 * qi * invL));
-    P[i] = make_float2((float)(qr * invL), (float)(qi * invL));
+    D[i] = C{(R)((s1 * qr - a) * invL), (R)(s1 * qi * invL)};
+    P[i] = C{(R)(qr * invL), (R)(qi * invL)};
   }
 }
 
+template <typename C>
 static int launch_coef(const bccb_plan_s* p, int mode, double s1, double a, const Workspace& w,
                        cudaStream_t st) {
   const int n = p->ax1.K * p->ax2.K;
   const double invL = 1.0 / ((double)p->L1 * (double)p->L2);
-  coef_kernel<<<(n + 255) / 256, 256, 0, st>>>(p->lam_box_dev, n, mode, s1, p->lam_out.real(), a,
-                                                invL, w.D, w.P);
+  ProfEvent* pe;
+  prof_before(KIND_OTHER, st, &pe);
+  coef_kernel<C><<<(n + 255) / 256, 256, 0, st>>>(p->lam_box_dev, n, mode, s1, p->lam_out.real(), a,
+                                                   invL, (C*)w.D, (C*)w.P);
+  prof_after(pe, st);
   LAUNCH_CHECK();
   return BCCB_OK;
 }
@@ -526,21 +637,31 @@ static int check_common(const bccb_plan_s* p, int batch, void* workspace) {
 }
 
 // ------------------------------------------------------------------ operator entry points
-extern "C" int bccb_matvec(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
-                           void* stream) {
+template <typename C>
+static int matvec_impl(bccb_plan_t p, int batch, const void* x, void* y, void* workspace, void* stream) {
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!x || !y) return fail(BCCB_ERR_INVALID, "x / y is NULL");
   DeviceGuard dg(p->device);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace w = carve(p, batch, workspace);
-  if ((rc = launch_coef(p, 0, 0.0, 0.0, w, st))) return rc;
-  EpiVector e{(const float2*)x, nullptr, nullptr, 0.f, 1.f};
-  if ((rc = launch_rows_vector(p, batch, false, true, w, e, st))) return rc;
-  if ((rc = launch_cols(p, batch, true, true, w, w.D, nullptr, nullptr, nullptr, st))) return rc;
-  const float lo = (float)p->lam_out.real();
-  EpiVector e2{(const float2*)x, (float2*)y, nullptr, lo, 1.f};
-  return launch_rows_vector(p, batch, true, false, w, e2, st);
+  using R = decltype(C::x);
+  if ((rc = launch_coef<C>(p, 0, 0.0, 0.0, w, st))) return rc;
+  EpiVector<C> e{(const C*)x, nullptr, nullptr, R(0), R(1)};
+  if ((rc = launch_rows_vector<C>(p, batch, false, true, w, e, st))) return rc;
+  if ((rc = launch_cols<C>(p, batch, true, true, w, (const C*)w.D, nullptr, nullptr, nullptr, st))) return rc;
+  EpiVector<C> e2{(const C*)x, (C*)y, nullptr, (R)p->lam_out.real(), R(1)};
+  return launch_rows_vector<C>(p, batch, true, false, w, e2, st);
+}
+
+extern "C" int bccb_matvec(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
+                           void* stream) {
+  return matvec_impl<float2>(p, batch, x, y, workspace, stream);
+}
+
+extern "C" int bccb_matvec_z(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
+                             void* stream) {
+  return matvec_impl<double2>(p, batch, x, y, workspace, stream);
 }
 
 extern "C" int bccb_spectrum_box(bccb_plan_t p, int batch, const void* x, void* out_box,
@@ -551,9 +672,9 @@ extern "C" int bccb_spectrum_box(bccb_plan_t p, int batch, const void* x, void* 
   DeviceGuard dg(p->device);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace w = carve(p, batch, workspace);
-  EpiVector e{(const float2*)x, nullptr, nullptr, 0.f, 1.f};
-  if ((rc = launch_rows_vector(p, batch, false, true, w, e, st))) return rc;
-  return launch_cols(p, batch, true, false, w, nullptr, nullptr, nullptr, (float2*)out_box, st);
+  EpiVector<float2> e{(const float2*)x, nullptr, nullptr, 0.f, 1.f};
+  if ((rc = launch_rows_vector<float2>(p, batch, false, true, w, e, st))) return rc;
+  return launch_cols<float2>(p, batch, true, false, w, nullptr, nullptr, nullptr, (float2*)out_box, st);
 }
 
 extern "C" int bccb_synthesize(bccb_plan_t p, int batch, const void* box, float scale, const void* x,
@@ -566,10 +687,10 @@ extern "C" int bccb_synthesize(bccb_plan_t p, int batch, const void* box, float 
   DeviceGuard dg(p->device);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace w = carve(p, batch, workspace);
-  if ((rc = launch_cols(p, batch, false, true, w, nullptr, nullptr, (const float2*)box, nullptr, st)))
+  if ((rc = launch_cols<float2>(p, batch, false, true, w, nullptr, nullptr, (const float2*)box, nullptr, st)))
     return rc;
-  EpiVector e{(const float2*)x, (float2*)out, maxabs, alpha, scale};
-  return launch_rows_vector(p, batch, true, false, w, e, st);
+  EpiVector<float2> e{(const float2*)x, (float2*)out, maxabs, alpha, scale};
+  return launch_rows_vector<float2>(p, batch, true, false, w, e, st);
 }
 
 // signed scatter of y into the spectral box: Bh[b][m1][m2] = L (-1)^(m1+m2) y[b][m]
@@ -606,17 +727,20 @@ extern "C" int bccb_adjoint(bccb_plan_t p, int batch, const void* y, void* bhat_
   CUDA_TRY(cudaMemsetAsync(bhat_box, 0, (size_t)batch * K1 * K2 * sizeof(float2), st));
   const long long total = (long long)batch * p->M;
   const float L = (float)((double)p->L1 * (double)p->L2);
+  ProfEvent* pe;
+  prof_before(KIND_OTHER, st, &pe);
   adjoint_scatter_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
       (const float2*)y, p->occ_dev, p->M, K1, K2, total, L, p->occ_alias, (float2*)bhat_box);
+  prof_after(pe, st);
   LAUNCH_CHECK();
   if (maxabs) CUDA_TRY(cudaMemsetAsync(maxabs, 0, (size_t)batch * sizeof(float), st));
   if (!b && !maxabs) return BCCB_OK;
   const float invL = (float)(1.0 / ((double)p->L1 * (double)p->L2));
-  if ((rc = launch_cols(p, batch, false, true, w, nullptr, nullptr, (const float2*)bhat_box, nullptr,
-                        st)))
+  if ((rc = launch_cols<float2>(p, batch, false, true, w, nullptr, nullptr, (const float2*)bhat_box,
+                                nullptr, st)))
     return rc;
-  EpiVector e{nullptr, (float2*)b, maxabs, 0.f, invL};
-  return launch_rows_vector(p, batch, true, false, w, e, st);
+  EpiVector<float2> e{nullptr, (float2*)b, maxabs, 0.f, invL};
+  return launch_rows_vector<float2>(p, batch, true, false, w, e, st);
 }
 
 // ------------------------------------------------------------------ solvers
@@ -626,7 +750,10 @@ __global__ void fill_int_kernel(int* p, int n, int v) {
 }
 
 static int reset_first_bad(int* first_bad, int batch, cudaStream_t st) {
+  ProfEvent* pe;
+  prof_before(KIND_OTHER, st, &pe);
   fill_int_kernel<<<(batch + 255) / 256, 256, 0, st>>>(first_bad, batch, INT_MAX);
+  prof_after(pe, st);
   LAUNCH_CHECK();
   return BCCB_OK;
 }
@@ -667,7 +794,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   cudaStream_t st = (cudaStream_t)stream;
   Workspace w = carve(p, batch, workspace);
   const double lo = p->lam_out.real();
-  if ((rc = launch_coef(p, 1, mu, 0.0, w, st))) return rc;
+  if ((rc = launch_coef<float2>(p, 1, mu, 0.0, w, st))) return rc;
   if (first_iteration == 0 && (rc = reset_first_bad(first_bad, batch, st))) return rc;
   EpiFista e;
   e.c = (double2*)c;
@@ -695,7 +822,8 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   e.beta_next = 0.0;
   if ((rc = launch_rows_fista(p, batch, false, true, w, e, st))) return rc;
   for (int t = first_iteration; t < t_end; ++t) {
-    if ((rc = launch_cols(p, batch, true, true, w, w.D, w.P, (const float2*)bhat_box, nullptr, st)))
+    if ((rc = launch_cols<float2>(p, batch, true, true, w, (const float2*)w.D, (const float2*)w.P,
+                                  (const float2*)bhat_box, nullptr, st)))
       return rc;
     e.it = t;
     e.beta_cur = e.momentum ? beta[t] : 0.0;
@@ -721,11 +849,11 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
   Workspace w = carve(p, batch, workspace);
   const double lo = p->lam_out.real();
   const double a = rho / (lo + rho);
-  if ((rc = launch_coef(p, 2, rho, a, w, st))) return rc;
+  if ((rc = launch_coef<double2>(p, 2, rho, a, w, st))) return rc;
   if (first_iteration == 0 && (rc = reset_first_bad(first_bad, batch, st))) return rc;
   EpiAdmm e;
   e.z = (float2*)z;
-  e.v = (float2*)v;
+  e.v = (double2*)v;
   e.c_out = nullptr;
   e.extra = (const float2*)extra;
   e.tau = tau;
@@ -737,10 +865,11 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
   const int t_end = first_iteration + iterations;
   if ((rc = launch_rows_admm(p, batch, false, true, w, e, st))) return rc;
   for (int t = first_iteration; t < t_end; ++t) {
-    if ((rc = launch_cols(p, batch, true, true, w, w.D, w.P, (const float2*)bhat_box, nullptr, st)))
+    if ((rc = launch_cols<double2>(p, batch, true, true, w, (const double2*)w.D, (const double2*)w.P,
+                                   (const float2*)bhat_box, nullptr, st)))
       return rc;
     e.it = t;
-    e.c_out = (t + 1 == t_end) ? (float2*)c_last : nullptr;
+    e.c_out = (t + 1 == t_end) ? (double2*)c_last : nullptr;
     if ((rc = launch_rows_admm(p, batch, true, t + 1 < t_end, w, e, st))) return rc;
   }
   return BCCB_OK;
@@ -766,6 +895,7 @@ extern "C" int bccb_topk(int batch, long long length, const void* values, int is
   const int kt = std::max(4, pow2_ceil(k));
 #define TOPK_CASE(KT)                                                                            \
   case KT:                                                                                       \
+    g_launches.fetch_add(2, std::memory_order_relaxed);                                          \
     topk_partial_kernel<KT><<<dim3(nchunk, batch), 256, 0, st>>>(values, is_double, length, k,   \
                                                                  nchunk, cand);                  \
     topk_merge_kernel<KT><<<batch, 256, 0, st>>>(cand, nchunk * k, k, idx, mag);                 \

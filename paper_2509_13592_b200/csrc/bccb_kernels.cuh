@@ -1,16 +1,16 @@
 // Pass kernels of the fused BCCB Gram iteration (sm_100a).
 //
 // One solver iteration = two launches:
-//   rows_kernel  (pass A, one L1-line per team): band inverse of V -> g, fused solver
-//                epilogue (gradient step + complex soft-threshold + FISTA momentum or
-//                ADMM z/v update + non-finite flag), band forward of the next operator
-//                input -> U.
-//   cols_kernel  (pass B, one L2-line per (snapshot, k1) team): band forward of U,
-//                spectral multiply-add  Y = D*X + P*Bhat  on the K2 x K1 box, band
-//                inverse -> V.
-// Intermediates U, V are [B][K1][L2] complex64 (transposed so pass B lines are
-// contiguous); Bhat / D / P boxes are [.][K1][K2].  The full-grid state never
-// leaves its [B][L2][L1] layout.  See DESIGN.md for the byte model.
+//   rows_*_kernel (pass A, one L1-line per team): band inverse of V -> g, fused solver
+//                 epilogue (gradient step + complex soft-threshold + FISTA momentum or
+//                 ADMM z/v update + non-finite flag), band forward of the next operator
+//                 input -> U.
+//   cols_kernel   (pass B, one L2-line per (snapshot, k1) team): band forward of U,
+//                 spectral multiply-add  Y = D*X + P*Bhat  on the K1 x K2 box, band
+//                 inverse -> V.
+// Intermediates U, V are [B][K1][L2] (transposed so pass-B lines are contiguous);
+// Bhat / D / P boxes are [.][K1][K2].  The full-grid state never leaves its
+// [B][L2][L1] layout.  See DESIGN.md for the byte model.
 #pragma once
 #include "band_fft.cuh"
 
@@ -25,26 +25,27 @@ struct Geo {
 
 // ------------------------------------------------------------------ epilogues
 // Every epilogue provides
-//   float2 load(pos, b)          : operator input x_t from the current state (first pass)
-//   float2 update(pos, b, g)     : consume g = (ifft2 part) at pos, update the state,
-//                                  return the next operator input x_{t+1}
+//   C load(pos, b)          : operator input x_t from the current state (first pass)
+//   ... update/step         : consume g (the ifft2 part) at pos, update the state and
+//                             return the next operator input x_{t+1}
 // `pos` is the flat index b*L + l2*L1 + l1; `b` the snapshot.
 
-// Plain input (matvec / spectrum of a user vector).  update() returns
-// out = alpha*x + scale*g; the kernel stores it and (optionally) reduces max|out|
-// per snapshot with one atomic per (warp, snapshot) group.
+// Plain vectors (matvec / spectrum / synthesis).  update() returns
+// out = alpha*x + scale*g; the kernel stores it and optionally reduces max|out|.
+template <typename C>
 struct EpiVector {
-  const float2* __restrict__ in;   // may be null when alpha == 0
-  float2* __restrict__ out;        // may be null (only maxabs wanted)
-  float* __restrict__ maxabs;      // may be null
-  float alpha, scale;
-  __device__ __forceinline__ float2 load(long long pos, int) const { return in[pos]; }
-  __device__ __forceinline__ float2 update(long long pos, int, float2 g) const {
-    float2 o = make_float2(scale * g.x, scale * g.y);
-    if (alpha != 0.f) {
-      const float2 x = in[pos];
-      o.x = fmaf(alpha, x.x, o.x);
-      o.y = fmaf(alpha, x.y, o.y);
+  using R = decltype(C::x);
+  const C* __restrict__ in;   // may be null when alpha == 0
+  C* __restrict__ out;        // may be null (only maxabs wanted)
+  float* __restrict__ maxabs; // may be null
+  R alpha, scale;
+  __device__ __forceinline__ C load(long long pos, int) const { return in[pos]; }
+  __device__ __forceinline__ C update(long long pos, int, C g) const {
+    C o = cmake(scale * g.x, scale * g.y);
+    if (alpha != R(0)) {
+      const C x = in[pos];
+      o.x = fma(alpha, x.x, o.x);
+      o.y = fma(alpha, x.y, o.y);
     }
     if (out) out[pos] = o;
     return o;
@@ -57,8 +58,7 @@ __device__ __forceinline__ void group_atomic_max(float* maxabs, int b, float m) 
   const unsigned act = __activemask();
   const unsigned grp = __match_any_sync(act, b);
   const unsigned v = __reduce_max_sync(grp, __float_as_uint(m));
-  if ((threadIdx.x & 31) == (__ffs(grp) - 1))
-    atomicMax(reinterpret_cast<unsigned int*>(maxabs) + b, v);
+  if ((threadIdx.x & 31) == (__ffs(grp) - 1)) atomicMax(reinterpret_cast<unsigned int*>(maxabs) + b, v);
 }
 
 // ISTA (momentum=false) and FISTA (momentum=true).
@@ -120,33 +120,34 @@ struct EpiFista {
   }
 };
 
-// ADMM: state z, v (complex64).  u = z - v is the operator input;
-// c = a*u + g (+extra) ; z' = S_kappa(c + v) ; v' = v + (c - z') ; u' = z' - v'.
-// reference: pkg/src/bccblasso/solvers.py:385-448 (loop 426-436).
+// ADMM (complex128 engine): state z (complex64), v (complex128).
+// u = z - v is the operator input; c = a*u + g (+extra); z' = S_kappa(c + v);
+// v' = v + (c - z'); u' = z' - v'.   reference: pkg/src/bccblasso/solvers.py:385-448.
 struct EpiAdmm {
   float2* z;
-  float2* v;
-  float2* c_out;                   // optional: c of this iteration (last iteration only)
+  double2* v;
+  double2* c_out;                  // optional: c of this iteration (last iteration only)
   const float2* __restrict__ extra;
   const double* __restrict__ tau;
   int* first_bad;
   double a, kscale, extra_scale;
   int it;
-  __device__ __forceinline__ float2 load(long long pos, int) const {
-    const float2 zz = z[pos], vv = v[pos];
-    return make_float2(zz.x - vv.x, zz.y - vv.y);
+  __device__ __forceinline__ double2 load(long long pos, int) const {
+    const float2 zz = z[pos];
+    const double2 vv = v[pos];
+    return make_double2((double)zz.x - vv.x, (double)zz.y - vv.y);
   }
-  __device__ __forceinline__ float2 step(float2 zz, float2 vv, float2 g, float2 e, int b,
-                                         float2& zn, float2& vn, float2& cc) const {
-    const double ur = (double)zz.x - (double)vv.x, ui = (double)zz.y - (double)vv.y;
-    double cr = __fma_rn(a, ur, (double)g.x);
-    double ci = __fma_rn(a, ui, (double)g.y);
+  __device__ __forceinline__ double2 step(float2 zz, double2 vv, double2 g, float2 e, int b,
+                                          float2& zn, double2& vn, double2& cc) const {
+    const double ur = (double)zz.x - vv.x, ui = (double)zz.y - vv.y;
+    double cr = __fma_rn(a, ur, g.x);
+    double ci = __fma_rn(a, ui, g.y);
     if (extra) {
       cr = __fma_rn(extra_scale, (double)e.x, cr);
       ci = __fma_rn(extra_scale, (double)e.y, ci);
     }
     if (!isfinite(cr) || !isfinite(ci)) atomicMin(first_bad + b, it);
-    const double sr = cr + (double)vv.x, si = ci + (double)vv.y;
+    const double sr = cr + vv.x, si = ci + vv.y;
     const double kap = kscale * tau[b];
     const double m2 = sr * sr + si * si;
     double nzr, nzi;
@@ -158,23 +159,25 @@ struct EpiAdmm {
       nzr = sr * f;
       nzi = si * f;
     }
-    const double nvr = (double)vv.x + (cr - nzr), nvi = (double)vv.y + (ci - nzi);
     zn = make_float2((float)nzr, (float)nzi);
-    vn = make_float2((float)nvr, (float)nvi);
-    cc = make_float2((float)cr, (float)ci);
-    return make_float2(zn.x - vn.x, zn.y - vn.y);
+    // v' = v + (c - z') on the stored z, so the reference identity
+    // v_t = v_{t-1} + (c_t - z_t) (pkg/tests/test_solvers.py:283-295) holds bitwise in float64.
+    vn = make_double2(vv.x + (cr - (double)zn.x), vv.y + (ci - (double)zn.y));
+    cc = make_double2(cr, ci);
+    return make_double2((double)zn.x - vn.x, (double)zn.y - vn.y);
   }
 };
 
-// ------------------------------------------------------------------ pass A
+// ------------------------------------------------------------------ pass A helpers
+template <typename C>
 struct RowsIO {
-  const float2* __restrict__ V;  // [B][K1][L2]  (inverse input)
-  float2* __restrict__ U;        // [B][K1][L2]  (forward output)
+  const C* __restrict__ V;  // [B][K1][L2]  (inverse input)
+  C* __restrict__ U;        // [B][K1][L2]  (forward output)
 };
 
-template <int KP>
-__device__ __forceinline__ void rows_load_band(const Geo& G, const Axis& ax, const RowsIO& io,
-                                               float2* Xs, long long row0) {
+template <typename C>
+__device__ __forceinline__ void rows_load_band(const Geo& G, const AxisT<C>& ax, const RowsIO<C>& io,
+                                               C* Xs, long long row0) {
   const int K = ax.K, TR = G.TR, XP = K + 1;
   for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
     const int k = idx / TR, ii = idx - k * TR;
@@ -186,10 +189,10 @@ __device__ __forceinline__ void rows_load_band(const Geo& G, const Axis& ax, con
   }
 }
 
-template <int KP>
-__device__ __forceinline__ void rows_forward_store(const Geo& G, const Axis& ax, const RowsIO& io,
-                                                   float2 (&a)[KP], bool active, int ii_self, int s,
-                                                   float2* Xs, float2* S, long long row0) {
+template <int KP, typename C>
+__device__ __forceinline__ void rows_forward_store(const Geo& G, const AxisT<C>& ax, const RowsIO<C>& io,
+                                                   C (&a)[KP], bool active, int ii_self, int s, C* Xs,
+                                                   C* S, long long row0) {
   const int K = ax.K, TR = G.TR, XP = K + 1;
   const int SP = KP * ax.pitch;  // per-line transpose buffer size
   if (active) {
@@ -212,20 +215,22 @@ __device__ __forceinline__ void rows_forward_store(const Geo& G, const Axis& ax,
   }
 }
 
+// ------------------------------------------------------------------ pass A kernels
 // Generic pass A for plain-vector epilogues.
-template <int KP>
-__global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, Axis ax, RowsIO io, EpiVector epi) {
-  extern __shared__ float2 smem[];
+template <int KP, typename C>
+__global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, AxisT<C> ax, RowsIO<C> io, EpiVector<C> epi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
   const int R = ax.R, K = ax.K;
   const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
   const long long row0 = (long long)blockIdx.x * G.TR;
   const long long gr = row0 + ii;
   const bool active = (ii < G.TR) && (gr < G.rows);
-  float2* Xs = smem;
-  float2* S = smem + G.TR * (K + 1);
-  float2 a[KP];
+  C* Xs = smem;
+  C* S = smem + G.TR * (K + 1);
+  C a[KP];
   if (G.do_inv) {
-    rows_load_band<KP>(G, ax, io, Xs, row0);
+    rows_load_band(G, ax, io, Xs, row0);
     __syncthreads();
     if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
   }
@@ -237,21 +242,23 @@ __global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, Axis ax, RowsIO
     for (int r = 0; r < KP; ++r) {
       const long long pos = base + (long long)R * r;
       a[r] = G.do_inv ? epi.update(pos, b, a[r]) : epi.load(pos, b);
-      mx = fmaxf(mx, sqrtf(a[r].x * a[r].x + a[r].y * a[r].y));
+      mx = fmaxf(mx, (float)sqrt((double)a[r].x * a[r].x + (double)a[r].y * a[r].y));
     }
     if (G.do_inv && epi.maxabs) group_atomic_max(epi.maxabs, b, mx);
   }
   if (G.do_fwd) {
-    if (G.do_inv) __syncthreads();  // Xs reuse
+    if (G.do_inv) __syncthreads();
     rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
   }
 }
 
-// Pass A for ISTA / FISTA with a software-pipelined state stream (loads of the
-// next chunk are issued before the stores of the current one; state is in place).
+// Pass A for ISTA / FISTA (complex64 engine) with a software-pipelined state stream:
+// loads of the next chunk are issued before the stores of the current one (in place).
 template <int KP, int CH>
-__global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, Axis ax, RowsIO io, EpiFista epi) {
-  extern __shared__ float2 smem[];
+__global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
+                                                         EpiFista epi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* smem = reinterpret_cast<float2*>(smem_raw);
   const int R = ax.R, K = ax.K;
   const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
   const long long row0 = (long long)blockIdx.x * G.TR;
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, Axis ax, RowsIO 
   float2* S = smem + G.TR * (K + 1);
   float2 a[KP];
   if (G.do_inv) {
-    rows_load_band<KP>(G, ax, io, Xs, row0);
+    rows_load_band(G, ax, io, Xs, row0);
     __syncthreads();
     if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
   }
@@ -320,19 +327,22 @@ __global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, Axis ax, RowsIO 
   }
 }
 
+// Pass A for ADMM (complex128 engine).
 template <int KP, int CH>
-__global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, Axis ax, RowsIO io, EpiAdmm epi) {
-  extern __shared__ float2 smem[];
+__global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, AxisT<double2> ax, RowsIO<double2> io,
+                                                        EpiAdmm epi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
   const int R = ax.R, K = ax.K;
   const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
   const long long row0 = (long long)blockIdx.x * G.TR;
   const long long gr = row0 + ii;
   const bool active = (ii < G.TR) && (gr < G.rows);
-  float2* Xs = smem;
-  float2* S = smem + G.TR * (K + 1);
-  float2 a[KP];
+  double2* Xs = smem;
+  double2* S = smem + G.TR * (K + 1);
+  double2 a[KP];
   if (G.do_inv) {
-    rows_load_band<KP>(G, ax, io, Xs, row0);
+    rows_load_band(G, ax, io, Xs, row0);
     __syncthreads();
     if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
   }
@@ -343,7 +353,8 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, Axis ax, RowsIO i
 #pragma unroll
       for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
     } else {
-      float2 zb[CH], vb[CH], eb[CH];
+      float2 zb[CH], eb[CH];
+      double2 vb[CH];
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
         const long long pos = base + (long long)R * q;
@@ -353,7 +364,8 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, Axis ax, RowsIO i
       }
 #pragma unroll
       for (int r0 = 0; r0 < KP; r0 += CH) {
-        float2 zn[CH], vn[CH], en[CH];
+        float2 zn[CH], en[CH];
+        double2 vn[CH];
         if (r0 + CH < KP) {
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
@@ -366,7 +378,8 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, Axis ax, RowsIO i
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
           const long long pos = base + (long long)R * (r0 + q);
-          float2 znew, vnew, cc;
+          float2 znew;
+          double2 vnew, cc;
           a[r0 + q] = epi.step(zb[q], vb[q], a[r0 + q], eb[q], b, znew, vnew, cc);
           epi.z[pos] = znew;
           epi.v[pos] = vnew;
@@ -390,32 +403,34 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, Axis ax, RowsIO i
 }
 
 // ------------------------------------------------------------------ pass B
+template <typename C>
 struct ColsIO {
-  const float2* __restrict__ U;     // [B][K1][L2] forward input (do_fwd)
-  float2* __restrict__ V;           // [B][K1][L2] inverse output (do_inv)
-  const float2* __restrict__ D;     // [K1][K2] multiplier (null => identity)
-  const float2* __restrict__ P;     // [K1][K2] rhs multiplier (null => 1)
-  const float2* __restrict__ Bh;    // [B][K1][K2] rhs box (null => none)
-  float2* __restrict__ box_out;     // [B][K1][K2] (used when !do_inv)
+  const C* __restrict__ U;          // [B][K1][L2] forward input (do_fwd)
+  C* __restrict__ V;                // [B][K1][L2] inverse output (do_inv)
+  const C* __restrict__ D;          // [K1][K2] multiplier (null => identity)
+  const C* __restrict__ P;          // [K1][K2] rhs multiplier (null => 1)
+  const float2* __restrict__ Bh;    // [B][K1][K2] rhs box, complex64 data (null => none)
+  C* __restrict__ box_out;          // [B][K1][K2] (used when !do_inv)
   int K1;
 };
 
 // One line = (snapshot b, column k1): length L2, band K2.
-template <int KP>
-__global__ void __launch_bounds__(256) cols_kernel(Geo G, Axis ax, ColsIO io) {
-  extern __shared__ float2 smem[];
+template <int KP, typename C>
+__global__ void __launch_bounds__(256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
   const int R = ax.R, K = ax.K, N = ax.N;
   const int TR = G.TR, XP = K + 1, SP = KP * ax.pitch;
   const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
   const long long row0 = (long long)blockIdx.x * TR;
   const long long gr = row0 + ii;
   const bool active = (ii < TR) && (gr < G.rows);
-  float2* Xs = smem;
-  float2* S = smem + TR * XP;
-  float2 a[KP];
+  C* Xs = smem;
+  C* S = smem + TR * XP;
+  C a[KP];
   if (G.do_fwd) {
     if (active) {
-      const float2* line = io.U + gr * N + s;
+      const C* line = io.U + gr * N + s;
 #pragma unroll
       for (int r = 0; r < KP; ++r) a[r] = line[(long long)R * r];
       reg_dft<KP, false>(a);
@@ -429,13 +444,13 @@ __global__ void __launch_bounds__(256) cols_kernel(Geo G, Axis ax, ColsIO io) {
     const long long g2 = row0 + i2;
     if (g2 >= G.rows) continue;
     const long long k1 = g2 % io.K1;
-    float2 y = make_float2(0.f, 0.f);
+    C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
     if (G.do_fwd) {
       y = band_fwd_output(S + i2 * SP, o, KP, ax);
       if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
     }
     if (io.Bh) {
-      float2 bh = io.Bh[g2 * K + o];
+      C bh = to_c(io.Bh[g2 * K + o], C{});
       if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
       y = cadd(y, bh);
     }
@@ -445,7 +460,7 @@ __global__ void __launch_bounds__(256) cols_kernel(Geo G, Axis ax, ColsIO io) {
   if (G.do_inv) {
     if (active) {
       band_inverse<KP>(Xs + ii * XP, s, ax, a);
-      float2* line = io.V + gr * N + s;
+      C* line = io.V + gr * N + s;
 #pragma unroll
       for (int r = 0; r < KP; ++r) line[(long long)R * r] = a[r];
     }

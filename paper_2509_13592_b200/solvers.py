@@ -408,14 +408,14 @@ def admm_solve(problem: LassoProblem, config: SolverConfig, iterate_callback=Non
     t0 = time.perf_counter()
     bhat, extra, tau_dev = problem.device_data()
     z = _initial_state(problem, config, torch.complex64)
-    v = torch.zeros_like(z)
+    v = torch.zeros(z.shape, dtype=torch.complex128, device=z.device)
     first_bad = torch.empty(problem.batch, dtype=torch.int32, device=z.device)
     ws = op.workspace(problem.batch)
     stream = _stream_ptr(op.device)
     record = config.record_objective
     y_norm = _require_y_norm(problem) if record else None
     slow = record or iterate_callback is not None
-    c_last = torch.empty_like(z) if slow else None
+    c_last = torch.empty_like(v) if slow else None
     precompute = time.perf_counter() - t0
     T = config.iterations
     trace = np.zeros((problem.batch, T if record else 0))
@@ -456,8 +456,8 @@ def admm_solve_with_c(problem: LassoProblem, config: SolverConfig):
     op = problem.gram
     bhat, extra, tau_dev = problem.device_data()
     z = _initial_state(problem, config, torch.complex64)
-    v = torch.zeros_like(z)
-    c_last = torch.empty_like(z)
+    v = torch.zeros(z.shape, dtype=torch.complex128, device=z.device)
+    c_last = torch.empty_like(v)
     first_bad = torch.empty(problem.batch, dtype=torch.int32, device=z.device)
     _lib.check(_lib.lib.bccb_admm_run(op._plan, problem.batch, 0, config.iterations, float(config.rho),
                                       tau_dev.data_ptr(), bhat.data_ptr(),
