@@ -8,6 +8,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -531,6 +532,45 @@ static int launch_rows_vector(const bccb_plan_s* p, int batch, bool inv, bool fw
   return BCCB_OK;
 }
 
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+constexpr int PIPE_STAGES = 8;
+
+template <int KP, bool MOM, bool EXTRA>
+static int launch_fista_pipe(const bccb_plan_s* p, const Geo& G, const AxisT<float2>& ax,
+                             const RowsIO<float2>& io, const EpiFista& epi, const LaunchShape& sh,
+                             cudaStream_t st) {
+  constexpr int CH = KP < 2 ? KP : 2;
+  constexpr int STG = PIPE_STAGES;
+  const long long tiles = (G.rows + G.TR - 1) / G.TR;
+  LaunchShape s2 = sh;
+  const size_t per = (size_t)STG * CH * sh.threads;
+  s2.smem += per * (sizeof(double2) + (MOM ? sizeof(float2) : 0) + (EXTRA ? sizeof(float2) : 0));
+  if (s2.smem > 227 * 1024) return -1;  // caller falls back to the register-pipelined kernel
+  const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)num_sms());
+  return launch_pass<float2>(rows_fista_pipe_kernel<KP, CH, STG, MOM, EXTRA>, KIND_ROWS, grid, s2, st, G, ax,
+                             io, epi, tiles);
+}
+
+// BCCB_ROWS_VARIANT: 0 = specialised shapes (default) else register-pipelined generic,
+// 1 = generic only, 2 = persistent cp.async ring.
+static int rows_variant() {
+  static int v = [] {
+    const char* e = getenv("BCCB_ROWS_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                              const EpiFista& epi, cudaStream_t st) {
   const LaunchShape sh = shape_for<float2>(p->ax1);
@@ -538,9 +578,45 @@ static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd
   RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   const AxisT<float2> ax = p->ax1.dev<float2>();
+  const bool mom = epi.momentum != 0, extra = epi.extra != nullptr;
+  // specialised shapes (compile-time KP, R, Mo); rows of a CTA must share one snapshot
+  if (!extra && G.rows < (1LL << 31) && p->L2 % sh.TR == 0 && sh.threads == 256 && rows_variant() != 1) {
+    const int key = ax.KP * 100000 + ax.R * 10 + ax.Mo;
+#define FAST_CASE(KP_, R_, MO_)                                                                          \
+  case KP_ * 100000 + R_ * 10 + MO_:                                                                     \
+    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true>, KIND_ROWS, grid, sh, st, G, \
+                                     ax, io, epi)                                                        \
+               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false>, KIND_ROWS, grid, sh, st,   \
+                                     G, ax, io, epi);
+    switch (key) {
+      FAST_CASE(16, 4, 1)    // L1 = 64,   band 16  (config 1)
+      FAST_CASE(32, 4, 1)    // L1 = 128,  band 32
+      FAST_CASE(32, 8, 1)    // L1 = 256,  band 32  (config 2)
+      FAST_CASE(32, 8, 2)    // L1 = 256,  band 64
+      FAST_CASE(32, 16, 2)   // L1 = 512,  band 64  (config 3 shape)
+      FAST_CASE(32, 16, 1)   // L1 = 512,  band 32
+      FAST_CASE(32, 32, 2)   // L1 = 1024, band 64  (config 4)
+      FAST_CASE(32, 32, 1)   // L1 = 1024, band 32
+      FAST_CASE(32, 64, 4)   // L1 = 2048, band 128
+      FAST_CASE(32, 128, 4)  // L1 = 4096, band 128 (config 5)
+      default:
+        break;
+    }
+#undef FAST_CASE
+  }
+  if (rows_variant() == 2 && inv) {
+    int rc = -1;
+    KP_DISPATCH_F(ax.KP, {
+      if (mom && !extra) rc = launch_fista_pipe<KPC, true, false>(p, G, ax, io, epi, sh, st);
+      else if (mom && extra) rc = launch_fista_pipe<KPC, true, true>(p, G, ax, io, epi, sh, st);
+      else if (!mom && !extra) rc = launch_fista_pipe<KPC, false, false>(p, G, ax, io, epi, sh, st);
+      else rc = launch_fista_pipe<KPC, false, true>(p, G, ax, io, epi, sh, st);
+    });
+    if (rc >= 0) return rc;
+  }
   KP_DISPATCH_F(ax.KP, {
-    constexpr int CH = KPC < 4 ? KPC : 4;
-    return launch_pass<float2>(rows_fista_kernel<KPC, CH>, KIND_ROWS, grid, sh, st, G, ax, io, epi);
+    constexpr int CH = KPC < 2 ? KPC : 2;
+    return launch_pass<float2>(rows_fista_kernel<KPC, CH, 2>, KIND_ROWS, grid, sh, st, G, ax, io, epi);
   });
   return BCCB_OK;
 }

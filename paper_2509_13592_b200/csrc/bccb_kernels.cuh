@@ -253,10 +253,13 @@ __global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, AxisT<C> ax, Ro
 }
 
 // Pass A for ISTA / FISTA (complex64 engine) with a software-pipelined state stream:
-// loads of the next chunk are issued before the stores of the current one (in place).
-template <int KP, int CH>
-__global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
-                                                         EpiFista epi) {
+// the first chunk of state is requested before the band inverse runs (its latency hides
+// behind the V-tile load and the inverse DFT), and every later chunk is requested before
+// the stores of the current one (state is updated in place).  MINB = CTAs per SM the
+// register allocation is capped for.
+template <int KP, int CH, int MINB>
+__global__ void __launch_bounds__(256, MINB) rows_fista_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
+                                                               EpiFista epi) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* smem = reinterpret_cast<float2*>(smem_raw);
   const int R = ax.R, K = ax.K;
@@ -267,27 +270,29 @@ __global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, AxisT<float2> ax
   float2* Xs = smem;
   float2* S = smem + G.TR * (K + 1);
   float2 a[KP];
+  const long long base = gr * G.L1 + s;
+  const int b = (int)(gr / G.L2);
+  double2 cb[CH];
+  float2 db[CH], eb[CH];
+  if (active && G.do_inv) {
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const long long pos = base + (long long)R * q;
+      cb[q] = epi.c[pos];
+      db[q] = epi.momentum ? epi.d[pos] : make_float2(0.f, 0.f);
+      eb[q] = epi.extra ? epi.extra[pos] : make_float2(0.f, 0.f);
+    }
+  }
   if (G.do_inv) {
     rows_load_band(G, ax, io, Xs, row0);
     __syncthreads();
     if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
   }
   if (active) {
-    const long long base = gr * G.L1 + s;
-    const int b = (int)(gr / G.L2);
     if (!G.do_inv) {
 #pragma unroll
       for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
     } else {
-      double2 cb[CH];
-      float2 db[CH], eb[CH];
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const long long pos = base + (long long)R * q;
-        cb[q] = epi.c[pos];
-        db[q] = epi.momentum ? epi.d[pos] : make_float2(0.f, 0.f);
-        eb[q] = epi.extra ? epi.extra[pos] : make_float2(0.f, 0.f);
-      }
 #pragma unroll
       for (int r0 = 0; r0 < KP; r0 += CH) {
         double2 cn[CH];
@@ -324,6 +329,291 @@ __global__ void __launch_bounds__(256) rows_fista_kernel(Geo G, AxisT<float2> ax
   if (G.do_fwd) {
     if (G.do_inv) __syncthreads();
     rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
+  }
+}
+
+// ---------------------------------------------------------------- pipelined pass A (FISTA/ISTA)
+// cp.async helpers (LDGSTS): per-thread asynchronous global->shared copies that hold no
+// registers while in flight.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Persistent pass A: every CTA walks row tiles blockIdx.x, +gridDim.x, ...; every thread
+// streams ITS OWN state elements (c: 16 B, d: 8 B) through a STAGES-deep ring of
+// CH-element chunks in shared memory.  The ring runs ahead across tile boundaries, so
+// the loads of tile k+1 are in flight while tile k does its band FFTs: the SM keeps
+// STAGES*CH*24 B per thread (~100 KB per SM) of reads outstanding without registers.
+// Shared memory: [Xs: TR x (K+1)] [S: TR x KP x pitch] [ring c] [ring d] [ring e].
+template <int KP, int CH, int STAGES, bool MOMENTUM, bool EXTRA>
+__global__ void __launch_bounds__(256, 1) rows_fista_pipe_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
+                                                                 EpiFista epi, long long num_tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NC = KP / CH;  // chunks per tile
+  const int R = ax.R, K = ax.K, TR = G.TR;
+  const int nthr = blockDim.x;
+  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
+  float2* Xs = reinterpret_cast<float2*>(smem_raw);
+  float2* S = Xs + TR * (K + 1);
+  double2* ring_c = reinterpret_cast<double2*>(S + TR * KP * ax.pitch);
+  float2* ring_d = reinterpret_cast<float2*>(ring_c + STAGES * CH * nthr);
+  float2* ring_e = ring_d + (MOMENTUM ? STAGES * CH * nthr : 0);
+  const long long step = gridDim.x;
+
+  // issue the copies of chunk `seq` of this thread's sequence into ring slot seq % STAGES
+  auto issue = [&](long long seq) {
+    const long long k = seq / NC;
+    const int ch = (int)(seq - k * NC);
+    const long long tile = blockIdx.x + k * step;
+    if (tile < num_tiles) {
+      const long long gr = tile * TR + ii;
+      if (ii < TR && gr < G.rows) {
+        const int slot = (int)(seq % STAGES);
+        const long long base = gr * G.L1 + s + (long long)R * (ch * CH);
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int si = (slot * CH + q) * nthr + threadIdx.x;
+          const long long pos = base + (long long)R * q;
+          cp_async16(ring_c + si, epi.c + pos);
+          if (MOMENTUM) cp_async8(ring_d + si, epi.d + pos);
+          if (EXTRA) cp_async8(ring_e + si, epi.extra + pos);
+        }
+      }
+    }
+    cp_async_commit();  // uniform group count, empty groups included
+  };
+
+  long long seq_next = 0;
+  if (G.do_inv)
+    for (int q = 0; q < STAGES - 1; ++q) issue(seq_next++);
+
+  long long seq = 0;
+  for (long long tile = blockIdx.x; tile < num_tiles; tile += step) {
+    const long long row0 = tile * TR;
+    const long long gr = row0 + ii;
+    const bool active = (ii < TR) && (gr < G.rows);
+    const long long base = gr * G.L1 + s;
+    const int b = (int)(gr / G.L2);
+    float2 a[KP];
+    if (G.do_inv) {
+      rows_load_band(G, ax, io, Xs, row0);
+      __syncthreads();
+      if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
+#pragma unroll
+      for (int ch = 0; ch < NC; ++ch, ++seq) {
+        issue(seq_next++);                 // keep STAGES-1 chunks ahead
+        cp_async_wait<STAGES - 1>();       // this thread's chunk `seq` has landed
+        if (active) {
+          const int slot = (int)(seq % STAGES);
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int si = (slot * CH + q) * nthr + threadIdx.x;
+            const int r = ch * CH + q;
+            const long long pos = base + (long long)R * r;
+            const double2 cc = ring_c[si];
+            const float2 dd = MOMENTUM ? ring_d[si] : make_float2(0.f, 0.f);
+            const float2 ee = EXTRA ? ring_e[si] : make_float2(0.f, 0.f);
+            double2 cnew;
+            float2 dnew;
+            a[r] = epi.step(cc, dd, a[r], ee, b, cnew, dnew);
+            epi.c[pos] = cnew;
+            if (MOMENTUM) epi.d[pos] = dnew;
+          }
+        }
+      }
+    } else if (active) {
+#pragma unroll
+      for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
+    }
+    if (G.do_fwd) {
+      __syncthreads();  // Xs / S reuse across tiles
+      rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------- specialised pass A (FISTA/ISTA)
+// Compile-time line shape: KP (register DFT), R (threads per line), MO (band / KP), so every
+// stride and loop bound is a constant.  Rows of a CTA never straddle snapshots (host checks
+// L2 % TR == 0), so all per-row scalars are hoisted and indices are 32-bit offsets from
+// per-row base pointers.
+//
+// Zero fast path (bitwise identical to the full update): when c_t = 0 and d_t = 0 the
+// operator input is x_t = 0, so w = g exactly; if fp32 |g|^2 is below kappa^2 by more than
+// its rounding bound the exact float64 test m2 <= kappa^2 must hold too, giving c_{t+1} = 0,
+// d_{t+1} = 0, x_{t+1} = 0 — state unchanged, so its stores are skipped.  After the first
+// few dozen iterations ~99% of the iterate is exactly zero (LASSO sparsity).
+template <int KP, int R, int MO, bool MOM>
+__global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
+                                                                 EpiFista epi) {
+  constexpr int TR = 256 / R;
+  constexpr int K = KP * MO;
+  constexpr int XP = K + 1;
+  constexpr int PITCH = (R % 2 == 1) ? R : R + 1;
+  constexpr int SP = KP * PITCH;
+  constexpr int CH = 2;
+  static_assert(KP % CH == 0, "chunking");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* Xs = reinterpret_cast<float2*>(smem_raw);
+  float2* S = Xs + TR * XP;
+  const int tid = threadIdx.x;
+  const int ii = tid / R, s = tid % R;
+  const int row0 = blockIdx.x * TR;            // rows < 2^31 (host check)
+  const int gr = row0 + ii;
+  const bool active = gr < (int)G.rows;
+  const int L2 = G.L2;
+  const int b = row0 / L2;                     // whole CTA lies in one snapshot
+  const int l20 = row0 - b * L2;
+  const long long vbase = (long long)b * K * L2 + l20;   // io.V/U index of (k=0, ii=0)
+  double2* cp = epi.c + (long long)gr * G.L1 + s;
+  float2* dp = MOM ? epi.d + (long long)gr * G.L1 + s : nullptr;
+  const double kap = epi.kscale * epi.tau[b];
+  const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
+  const double a_id = epi.a, bc = epi.beta_cur;
+  const float bn = (float)epi.beta_next;
+  float2 a[KP];
+
+  if (G.do_inv) {
+    // band tile V[b][k][l20 + ii] -> Xs[ii][k]
+#pragma unroll
+    for (int idx = tid; idx < TR * K; idx += 256) {
+      const int k = idx / TR, i2 = idx % TR;
+      Xs[i2 * XP + k] = io.V[vbase + (long long)k * L2 + i2];
+    }
+    // first state chunk in flight while the inverse DFT runs
+    double2 cb[CH];
+    float2 db[CH];
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        cb[q] = cp[q * R];
+        db[q] = MOM ? dp[q * R] : make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    if (active) {
+      // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT)
+      const float2* Y = Xs + ii * XP;
+#pragma unroll
+      for (int j = 0; j < KP; ++j) a[j] = Y[j];
+#pragma unroll
+      for (int m = 1; m < MO; ++m) {
+        const float2 w2 = __ldg(ax.tw2 + m * R + s);
+#pragma unroll
+        for (int j = 0; j < KP; ++j) a[j] = cadd(a[j], cmulc(Y[j + KP * m], w2));
+      }
+#pragma unroll
+      for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], __ldg(ax.tw1 + j * R + s));
+      reg_dft<KP, true>(a);
+      // ---- fused epilogue, register-pipelined state stream
+#pragma unroll
+      for (int r0 = 0; r0 < KP; r0 += CH) {
+        double2 cn[CH];
+        float2 dn[CH];
+        if (r0 + CH < KP) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            cn[q] = cp[(r0 + CH + q) * R];
+            dn[q] = MOM ? dp[(r0 + CH + q) * R] : make_float2(0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int r = r0 + q;
+          const float2 g = a[r];
+          const double2 cc = cb[q];
+          const float2 dd = db[q];
+          const bool zero_state = (cc.x == 0.0) & (cc.y == 0.0) & (!MOM | ((dd.x == 0.f) & (dd.y == 0.f)));
+          if (zero_state && fmaf(g.x, g.x, g.y * g.y) < kap2_lo) {
+            a[r] = make_float2(0.f, 0.f);   // c, d stay 0: no stores
+            continue;
+          }
+          double xr = cc.x, xi = cc.y;
+          if (MOM) {
+            xr = __fma_rn(bc, (double)dd.x, xr);
+            xi = __fma_rn(bc, (double)dd.y, xi);
+          }
+          const double wr = __fma_rn(a_id, xr, (double)g.x);
+          const double wi = __fma_rn(a_id, xi, (double)g.y);
+          if (!isfinite(wr + wi)) atomicMin(epi.first_bad + b, epi.it);
+          const double m2 = wr * wr + wi * wi;
+          double nr = 0.0, ni = 0.0;
+          if (!(m2 <= kap * kap)) {
+            const double f = 1.0 - kap * rsqrt(m2);
+            nr = wr * f;
+            ni = wi * f;
+          }
+          cp[r * R] = make_double2(nr, ni);
+          if (MOM) {
+            const float2 dnew = make_float2((float)(nr - cc.x), (float)(ni - cc.y));
+            dp[r * R] = dnew;
+            a[r] = make_float2(fmaf(bn, dnew.x, (float)nr), fmaf(bn, dnew.y, (float)ni));
+          } else {
+            a[r] = make_float2((float)nr, (float)ni);
+          }
+        }
+        if (r0 + CH < KP) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            cb[q] = cn[q];
+            db[q] = dn[q];
+          }
+        }
+      }
+    }
+  } else if (active) {
+#pragma unroll
+    for (int r = 0; r < KP; ++r) {
+      double2 cc = cp[r * R];
+      if (MOM) {
+        const float2 dd = dp[r * R];
+        cc.x = __fma_rn(bc, (double)dd.x, cc.x);
+        cc.y = __fma_rn(bc, (double)dd.y, cc.y);
+      }
+      a[r] = make_float2((float)cc.x, (float)cc.y);
+    }
+  }
+  if (!G.do_fwd) return;
+  // ---- band forward: register DFT, twiddle + transpose scatter, R-term reductions
+  if (active) {
+    reg_dft<KP, false>(a);
+    float2* Srow = S + ii * SP;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], __ldg(ax.tw1 + j * R + s));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int idx = tid; idx < TR * K; idx += 256) {
+    const int i2 = idx / K, o = idx % K;
+    const int j = o % KP, m = o / KP;
+    const float2* row = S + i2 * SP + j * PITCH;
+    float2 acc = make_float2(0.f, 0.f);
+    if (m == 0) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) acc = cadd(acc, row[t]);
+    } else {
+      const float2* tw = ax.tw2 + m * R;
+#pragma unroll
+      for (int t = 0; t < R; ++t) acc = cfma(row[t], __ldg(tw + t), acc);
+    }
+    Xs[i2 * XP + o] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int idx = tid; idx < TR * K; idx += 256) {
+    const int k = idx / TR, i2 = idx % TR;
+    if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
   }
 }
 
