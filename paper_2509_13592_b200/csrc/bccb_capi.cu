@@ -144,7 +144,9 @@ struct AxisPrec {
 
 struct AxisHost {
   int N = 0, K = 0;
-  AxisPrec f, d;  // complex64 engine (KP <= 32), complex128 engine (KP <= 16)
+  // complex64 engine (KP <= 32), complex128 engine (KP <= 16), complex64 column-pass engine
+  // (KP <= 16: more threads for the few, short column lines)
+  AxisPrec f, d, s;
   template <typename C>
   const AxisPrec& prec() const;
   template <typename C>
@@ -159,6 +161,18 @@ struct AxisHost {
     a.pitch = p.pitch;
     a.tw1 = (const C*)p.tw1;
     a.tw2 = (const C*)p.tw2;
+    return a;
+  }
+  AxisT<float2> dev_s() const {
+    AxisT<float2> a;
+    a.N = N;
+    a.K = K;
+    a.KP = s.KP;
+    a.R = s.R;
+    a.Mo = s.Mo;
+    a.pitch = s.pitch;
+    a.tw1 = (const float2*)s.tw1;
+    a.tw2 = (const float2*)s.tw2;
     return a;
   }
 };
@@ -218,9 +232,15 @@ static int make_axis(int N, int Kreq, AxisHost& ax) {
   if (K % KP != 0) K = N;  // N is a multiple of KP
   ax.N = N;
   ax.K = K;
-  const int kps[2] = {KP, std::min(KP, KP_MAX_D)};
-  AxisPrec* aps[2] = {&ax.f, &ax.d};
-  for (int q = 0; q < 2; ++q) {
+  // column-pass register DFT size (BCCB_COLS_KP overrides for tuning; default 16)
+  static const int cols_kp = [] {
+    const char* e = getenv("BCCB_COLS_KP");
+    const int v = e ? atoi(e) : 16;
+    return (v == 4 || v == 8 || v == 16 || v == 32) ? v : 16;
+  }();
+  const int kps[3] = {KP, std::min(KP, KP_MAX_D), std::min(KP, cols_kp)};
+  AxisPrec* aps[3] = {&ax.f, &ax.d, &ax.s};
+  for (int q = 0; q < 3; ++q) {
     AxisPrec& ap = *aps[q];
     ap.KP = kps[q];
     ap.R = N / ap.KP;
@@ -234,14 +254,15 @@ static int make_axis(int N, int Kreq, AxisHost& ax) {
   }
   int rc = upload_twiddles<float2>(N, ax.f);
   if (!rc) rc = upload_twiddles<double2>(N, ax.d);
+  if (!rc) rc = upload_twiddles<float2>(N, ax.s);
   return rc;
 }
 
 static void free_axis(AxisHost& a) {
-  cudaFree(a.f.tw1);
-  cudaFree(a.f.tw2);
-  cudaFree(a.d.tw1);
-  cudaFree(a.d.tw2);
+  for (AxisPrec* p : {&a.f, &a.d, &a.s}) {
+    cudaFree(p->tw1);
+    cudaFree(p->tw2);
+  }
 }
 
 static void free_plan(bccb_plan_s* p) {
@@ -418,14 +439,27 @@ struct Workspace {
   void* V;
   void* D;
   void* P;
+  unsigned char* flags;  // zero-segment flags of the streaming FISTA pass
 };
 
+// threads per CTA of the specialised FISTA rows pass (flags: one 32-bit word per warp)
+static int zs_threads(const AxisHost& ax) { return std::max(256, ax.f.R); }
+static size_t zs_flag_bytes(const bccb_plan_s* p, int batch);
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) {
+  const int nt = zs_threads(p->ax1);
+  const int tr = nt / p->ax1.f.R;
+  const long long rows = (long long)batch * p->L2;
+  const long long ctas = (rows + tr - 1) / tr;
+  return (size_t)ctas * (nt / 32) * sizeof(unsigned);
+}
 
 static size_t ws_bytes(const bccb_plan_s* p, int batch) {
   const size_t inter = (size_t)batch * p->ax1.K * p->L2 * sizeof(double2);
   const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
-  return 2 * align_up(inter) + 2 * align_up(box);
+  return 2 * align_up(inter) + 2 * align_up(box) + align_up(zs_flag_bytes(p, batch));
 }
 
 static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
@@ -440,6 +474,8 @@ static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   w.D = ptr;
   ptr += box;
   w.P = ptr;
+  ptr += box;
+  w.flags = (unsigned char*)ptr;
   return w;
 }
 
@@ -454,11 +490,25 @@ struct LaunchShape {
   size_t smem;
 };
 
+// Lines per CTA: 256 threads by default; when the launch would leave SMs idle (few lines,
+// e.g. the column pass of config 2: 2048 lines) shrink the CTA so the grid covers >= 2 waves.
+static LaunchShape shape_for_prec(const AxisHost& ax, const AxisPrec& ap, size_t elem, long long lines) {
+  LaunchShape s;
+  s.TR = std::max(1, 256 / ap.R);
+  if (lines > 0)
+    while (s.TR > 1 && s.TR * ap.R > 64 && (lines + s.TR - 1) / s.TR < 2 * 148) s.TR /= 2;
+  s.threads = s.TR * ap.R;
+  s.smem = ((size_t)s.TR * (ax.K + 1) + (size_t)s.TR * ap.KP * ap.pitch) * elem;
+  return s;
+}
+
 template <typename C>
-static LaunchShape shape_for(const AxisHost& ax) {
+static LaunchShape shape_for(const AxisHost& ax, long long lines = 0) {
   const AxisPrec& ap = ax.prec<C>();
   LaunchShape s;
   s.TR = std::max(1, 256 / ap.R);
+  if (lines > 0)
+    while (s.TR > 1 && s.TR * ap.R > 64 && (lines + s.TR - 1) / s.TR < 2 * 148) s.TR /= 2;
   s.threads = s.TR * ap.R;
   s.smem = ((size_t)s.TR * (ax.K + 1) + (size_t)s.TR * ap.KP * ap.pitch) * sizeof(C);
   return s;
@@ -571,6 +621,89 @@ static int rows_variant() {
   return v;
 }
 
+// Specialised line shapes (compile-time KP, R, Mo) of the FISTA/ISTA rows pass.
+#define FAST_SHAPES(X)                                                \
+  X(16, 4, 1)    /* L1 = 64,   band 16  (config 1) */                 \
+  X(32, 4, 1)    /* L1 = 128,  band 32 */                             \
+  X(32, 8, 1)    /* L1 = 256,  band 32  (config 2) */                 \
+  X(32, 8, 2)    /* L1 = 256,  band 64 */                             \
+  X(32, 16, 1)   /* L1 = 512,  band 32 */                             \
+  X(32, 16, 2)   /* L1 = 512,  band 64  (config 3 shape) */           \
+  X(32, 32, 1)   /* L1 = 1024, band 32 */                             \
+  X(32, 32, 2)   /* L1 = 1024, band 64  (config 4) */                 \
+  X(32, 64, 4)   /* L1 = 2048, band 128 */                            \
+  X(32, 128, 4)  /* L1 = 4096, band 128 (config 5) */
+
+static int fast_key(const AxisPrec& a) { return a.KP * 100000 + a.R * 10 + a.Mo; }
+
+static bool fast_supported(const bccb_plan_s* p, int batch, const void* extra) {
+  if (extra || rows_variant() != 0) return false;
+  const AxisPrec& a = p->ax1.f;
+  const int tr = zs_threads(p->ax1) / a.R;
+  if ((long long)batch * p->L2 >= (1LL << 31) || p->L2 % tr != 0) return false;
+  const int key = fast_key(a);
+#define FAST_KEY(KP_, R_, MO_) \
+  if (key == KP_ * 100000 + R_ * 10 + MO_) return true;
+  FAST_SHAPES(FAST_KEY)
+#undef FAST_KEY
+  return false;
+}
+
+static LaunchShape fast_shape(const bccb_plan_s* p) {
+  const AxisPrec& a = p->ax1.f;
+  LaunchShape sh;
+  sh.threads = zs_threads(p->ax1);
+  sh.TR = sh.threads / a.R;
+  const int pitch = (a.R % 2 == 1) ? a.R : a.R + 1;
+  sh.smem = ((size_t)sh.TR * (p->ax1.K + 1) + (size_t)sh.TR * a.KP * pitch) * sizeof(float2);
+  return sh;
+}
+
+static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
+                                  const EpiFista& epi, bool zs, cudaStream_t st) {
+  const LaunchShape sh = fast_shape(p);
+  const Geo G = rows_geo(p, batch, sh, inv, fwd);
+  RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const AxisT<float2> ax = p->ax1.dev<float2>();
+  const bool mom = epi.momentum != 0;
+  unsigned* fl = (unsigned*)w.flags;
+  const int key = fast_key(p->ax1.f);
+#define FAST_CASE(KP_, R_, MO_)                                                                              \
+  if (key == KP_ * 100000 + R_ * 10 + MO_) {                                                                 \
+    if (zs)                                                                                                  \
+      return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true>, KIND_ROWS, grid, sh, st, \
+                                       G, ax, io, epi, fl)                                                   \
+                 : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true>, KIND_ROWS, grid, sh,   \
+                                       st, G, ax, io, epi, fl);                                              \
+    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, false>, KIND_ROWS, grid, sh, st,  \
+                                     G, ax, io, epi, fl)                                                     \
+               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, false>, KIND_ROWS, grid, sh, st, \
+                                     G, ax, io, epi, fl);                                                    \
+  }
+  FAST_SHAPES(FAST_CASE)
+#undef FAST_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
+}
+
+static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace& w, double2* c, float2* d,
+                                cudaStream_t st) {
+  LaunchShape sh = fast_shape(p);
+  const Geo G = rows_geo(p, batch, sh, false, false);
+  sh.smem = 0;
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const int key = fast_key(p->ax1.f);
+  const unsigned* fl = (const unsigned*)w.flags;
+#define ZERO_CASE(KP_, R_, MO_)                                                                           \
+  if (key == KP_ * 100000 + R_ * 10 + MO_)                                                                \
+    return launch_pass<float2>(zero_segments_kernel<KP_, R_>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+  FAST_SHAPES(ZERO_CASE)
+#undef ZERO_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
+}
+
+// Generic rows pass (runtime line shape): register-pipelined kernel, or the persistent cp.async
+// ring with BCCB_ROWS_VARIANT=2.
 static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                              const EpiFista& epi, cudaStream_t st) {
   const LaunchShape sh = shape_for<float2>(p->ax1);
@@ -579,31 +712,6 @@ static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   const AxisT<float2> ax = p->ax1.dev<float2>();
   const bool mom = epi.momentum != 0, extra = epi.extra != nullptr;
-  // specialised shapes (compile-time KP, R, Mo); rows of a CTA must share one snapshot
-  if (!extra && G.rows < (1LL << 31) && p->L2 % sh.TR == 0 && sh.threads == 256 && rows_variant() != 1) {
-    const int key = ax.KP * 100000 + ax.R * 10 + ax.Mo;
-#define FAST_CASE(KP_, R_, MO_)                                                                          \
-  case KP_ * 100000 + R_ * 10 + MO_:                                                                     \
-    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true>, KIND_ROWS, grid, sh, st, G, \
-                                     ax, io, epi)                                                        \
-               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false>, KIND_ROWS, grid, sh, st,   \
-                                     G, ax, io, epi);
-    switch (key) {
-      FAST_CASE(16, 4, 1)    // L1 = 64,   band 16  (config 1)
-      FAST_CASE(32, 4, 1)    // L1 = 128,  band 32
-      FAST_CASE(32, 8, 1)    // L1 = 256,  band 32  (config 2)
-      FAST_CASE(32, 8, 2)    // L1 = 256,  band 64
-      FAST_CASE(32, 16, 2)   // L1 = 512,  band 64  (config 3 shape)
-      FAST_CASE(32, 16, 1)   // L1 = 512,  band 32
-      FAST_CASE(32, 32, 2)   // L1 = 1024, band 64  (config 4)
-      FAST_CASE(32, 32, 1)   // L1 = 1024, band 32
-      FAST_CASE(32, 64, 4)   // L1 = 2048, band 128
-      FAST_CASE(32, 128, 4)  // L1 = 4096, band 128 (config 5)
-      default:
-        break;
-    }
-#undef FAST_CASE
-  }
   if (rows_variant() == 2 && inv) {
     int rc = -1;
     KP_DISPATCH_F(ax.KP, {
@@ -638,7 +746,10 @@ static int launch_rows_admm(const bccb_plan_s* p, int batch, bool inv, bool fwd,
 template <typename C>
 static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, const Workspace& w,
                        const C* D, const C* P, const float2* Bh, C* box_out, cudaStream_t st) {
-  const LaunchShape sh = shape_for<C>(p->ax2);
+  // complex64 columns run the streaming (KP <= 8) axis: many more threads for few lines
+  const bool stream_axis = std::is_same<C, float2>::value;
+  const LaunchShape sh = stream_axis ? shape_for_prec(p->ax2, p->ax2.s, sizeof(C), (long long)batch * p->ax1.K)
+                                     : shape_for<C>(p->ax2, (long long)batch * p->ax1.K);
   Geo G;
   G.L1 = p->L1;
   G.L2 = p->L2;
@@ -655,10 +766,11 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   io.box_out = box_out;
   io.K1 = p->ax1.K;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  const AxisT<C> ax = p->ax2.dev<C>();
   if constexpr (std::is_same<C, float2>::value) {
+    const AxisT<C> ax = p->ax2.dev_s();
     KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
   } else {
+    const AxisT<C> ax = p->ax2.dev<C>();
     KP_DISPATCH_D(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
   }
   return BCCB_OK;
@@ -896,7 +1008,15 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   e.it = first_iteration;
   e.beta_cur = e.momentum ? beta[first_iteration] : 0.0;
   e.beta_next = 0.0;
-  if ((rc = launch_rows_fista(p, batch, false, true, w, e, st))) return rc;
+  // specialised shapes use zero-segment skipping: flags start all-ones (read everything) and
+  // the skipped zeros are written back by one final pass
+  const bool zs = fast_supported(p, batch, extra);
+  auto rows = [&](bool inv, bool fwd) {
+    return zs ? launch_rows_fista_fast(p, batch, inv, fwd, w, e, true, st)
+              : launch_rows_fista(p, batch, inv, fwd, w, e, st);
+  };
+  if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes(p, batch), st));
+  if ((rc = rows(false, true))) return rc;
   for (int t = first_iteration; t < t_end; ++t) {
     if ((rc = launch_cols<float2>(p, batch, true, true, w, (const float2*)w.D, (const float2*)w.P,
                                   (const float2*)bhat_box, nullptr, st)))
@@ -904,8 +1024,9 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
     e.it = t;
     e.beta_cur = e.momentum ? beta[t] : 0.0;
     e.beta_next = e.momentum ? beta[t + 1] : 0.0;
-    if ((rc = launch_rows_fista(p, batch, true, t + 1 < t_end, w, e, st))) return rc;
+    if ((rc = rows(true, t + 1 < t_end))) return rc;
   }
+  if (zs && (rc = launch_zero_segments(p, batch, w, (double2*)c, (float2*)d, st))) return rc;
   return BCCB_OK;
 }
 

@@ -454,10 +454,16 @@ __global__ void __launch_bounds__(256, 1) rows_fista_pipe_kernel(Geo G, AxisT<fl
 // its rounding bound the exact float64 test m2 <= kappa^2 must hold too, giving c_{t+1} = 0,
 // d_{t+1} = 0, x_{t+1} = 0 — state unchanged, so its stores are skipped.  After the first
 // few dozen iterations ~99% of the iterate is exactly zero (LASSO sparsity).
-template <int KP, int R, int MO, bool MOM>
-__global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
-                                                                 EpiFista epi) {
-  constexpr int TR = 256 / R;
+//
+// Zero-segment skipping (ZS): flags[warp] bit r says whether the 32 state elements held by
+// the warp's lanes at register slot r may be nonzero.  Clear segments are not read (they are
+// exactly zero) and not written while they stay zero; a segment that is (or becomes) nonzero
+// is written whole.  zero_segments_kernel writes the skipped zeros back at the end of a run.
+template <int KP, int R, int MO, bool MOM, bool ZS>
+__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
+    rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags) {
+  constexpr int NT = R > 256 ? R : 256;   // threads per CTA
+  constexpr int TR = NT / R;
   constexpr int K = KP * MO;
   constexpr int XP = K + 1;
   constexpr int PITCH = (R % 2 == 1) ? R : R + 1;
@@ -482,27 +488,29 @@ __global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<fl
   const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
   const double a_id = epi.a, bc = epi.beta_cur;
   const float bn = (float)epi.beta_next;
+  const int lane = tid & 31;
+  unsigned* fw = ZS ? flags + ((long long)blockIdx.x * (NT / 32) + (tid >> 5)) : nullptr;
+  const unsigned fl = ZS ? *fw : 0xffffffffu;
   float2 a[KP];
 
   if (G.do_inv) {
     // band tile V[b][k][l20 + ii] -> Xs[ii][k]
-#pragma unroll
-    for (int idx = tid; idx < TR * K; idx += 256) {
+    for (int idx = tid; idx < TR * K; idx += NT) {
       const int k = idx / TR, i2 = idx % TR;
       Xs[i2 * XP + k] = io.V[vbase + (long long)k * L2 + i2];
     }
     // first state chunk in flight while the inverse DFT runs
     double2 cb[CH];
     float2 db[CH];
-    if (active) {
 #pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        cb[q] = cp[q * R];
-        db[q] = MOM ? dp[q * R] : make_float2(0.f, 0.f);
-      }
+    for (int q = 0; q < CH; ++q) {
+      const bool live = active && ((fl >> q) & 1u);
+      cb[q] = live ? cp[q * R] : make_double2(0.0, 0.0);
+      db[q] = (MOM && live) ? dp[q * R] : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    if (active) {
+    unsigned nfl = 0;
+    {
       // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT)
       const float2* Y = Xs + ii * XP;
 #pragma unroll
@@ -524,8 +532,9 @@ __global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<fl
         if (r0 + CH < KP) {
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
-            cn[q] = cp[(r0 + CH + q) * R];
-            dn[q] = MOM ? dp[(r0 + CH + q) * R] : make_float2(0.f, 0.f);
+            const bool live = active && ((fl >> (r0 + CH + q)) & 1u);
+            cn[q] = live ? cp[(r0 + CH + q) * R] : make_double2(0.0, 0.0);
+            dn[q] = (MOM && live) ? dp[(r0 + CH + q) * R] : make_float2(0.f, 0.f);
           }
         }
 #pragma unroll
@@ -535,33 +544,44 @@ __global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<fl
           const double2 cc = cb[q];
           const float2 dd = db[q];
           const bool zero_state = (cc.x == 0.0) & (cc.y == 0.0) & (!MOM | ((dd.x == 0.f) & (dd.y == 0.f)));
-          if (zero_state && fmaf(g.x, g.x, g.y * g.y) < kap2_lo) {
-            a[r] = make_float2(0.f, 0.f);   // c, d stay 0: no stores
-            continue;
-          }
-          double xr = cc.x, xi = cc.y;
-          if (MOM) {
-            xr = __fma_rn(bc, (double)dd.x, xr);
-            xi = __fma_rn(bc, (double)dd.y, xi);
-          }
-          const double wr = __fma_rn(a_id, xr, (double)g.x);
-          const double wi = __fma_rn(a_id, xi, (double)g.y);
-          if (!isfinite(wr + wi)) atomicMin(epi.first_bad + b, epi.it);
-          const double m2 = wr * wr + wi * wi;
           double nr = 0.0, ni = 0.0;
-          if (!(m2 <= kap * kap)) {
-            const double f = 1.0 - kap * rsqrt(m2);
-            nr = wr * f;
-            ni = wi * f;
+          float2 dnew = make_float2(0.f, 0.f);
+          bool nz = false;
+          if (active && !(zero_state && fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
+            double xr = cc.x, xi = cc.y;
+            if (MOM) {
+              xr = __fma_rn(bc, (double)dd.x, xr);
+              xi = __fma_rn(bc, (double)dd.y, xi);
+            }
+            const double wr = __fma_rn(a_id, xr, (double)g.x);
+            const double wi = __fma_rn(a_id, xi, (double)g.y);
+            if (!isfinite(wr + wi)) atomicMin(epi.first_bad + b, epi.it);
+            const double m2 = wr * wr + wi * wi;
+            if (!(m2 <= kap * kap)) {
+              const double f = 1.0 - kap * rsqrt(m2);
+              nr = wr * f;
+              ni = wi * f;
+            }
+            if (MOM) dnew = make_float2((float)(nr - cc.x), (float)(ni - cc.y));
+            nz = true;   // state touched: value may be nonzero or may have changed
+            if (!ZS) {
+              cp[r * R] = make_double2(nr, ni);
+              if (MOM) dp[r * R] = dnew;
+            }
           }
-          cp[r * R] = make_double2(nr, ni);
-          if (MOM) {
-            const float2 dnew = make_float2((float)(nr - cc.x), (float)(ni - cc.y));
-            dp[r * R] = dnew;
-            a[r] = make_float2(fmaf(bn, dnew.x, (float)nr), fmaf(bn, dnew.y, (float)ni));
-          } else {
-            a[r] = make_float2((float)nr, (float)ni);
+          if (ZS) {
+            const bool nzv = (nr != 0.0) | (ni != 0.0) | (MOM & ((dnew.x != 0.f) | (dnew.y != 0.f)));
+            if (__any_sync(0xffffffffu, nzv)) {  // segment (still / newly) nonzero: write it whole
+              if (active) {
+                cp[r * R] = make_double2(nr, ni);
+                if (MOM) dp[r * R] = dnew;
+              }
+              nfl |= 1u << r;
+            }
           }
+          (void)nz;
+          a[r] = MOM ? make_float2(fmaf(bn, dnew.x, (float)nr), fmaf(bn, dnew.y, (float)ni))
+                     : make_float2((float)nr, (float)ni);
         }
         if (r0 + CH < KP) {
 #pragma unroll
@@ -572,9 +592,14 @@ __global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<fl
         }
       }
     }
+    if (ZS && lane == 0) *fw = nfl;
   } else if (active) {
 #pragma unroll
     for (int r = 0; r < KP; ++r) {
+      if (!((fl >> r) & 1u)) {
+        a[r] = make_float2(0.f, 0.f);
+        continue;
+      }
       double2 cc = cp[r * R];
       if (MOM) {
         const float2 dd = dp[r * R];
@@ -593,8 +618,7 @@ __global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<fl
     for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], __ldg(ax.tw1 + j * R + s));
   }
   __syncthreads();
-#pragma unroll
-  for (int idx = tid; idx < TR * K; idx += 256) {
+  for (int idx = tid; idx < TR * K; idx += NT) {
     const int i2 = idx / K, o = idx % K;
     const int j = o % KP, m = o / KP;
     const float2* row = S + i2 * SP + j * PITCH;
@@ -610,11 +634,32 @@ __global__ void __launch_bounds__(256, 2) rows_fista_fast_kernel(Geo G, AxisT<fl
     Xs[i2 * XP + o] = acc;
   }
   __syncthreads();
-#pragma unroll
-  for (int idx = tid; idx < TR * K; idx += 256) {
+  for (int idx = tid; idx < TR * K; idx += NT) {
     const int k = idx / TR, i2 = idx % TR;
     if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
   }
+}
+
+// Final pass of a zero-skipping run: write the zeros of every clear segment back so c (and d)
+// are dense, consistent arrays again.
+template <int KP, int R>
+__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G, double2* c, float2* d,
+                                                                          const unsigned* __restrict__ flags) {
+  constexpr int NT = R > 256 ? R : 256;
+  constexpr int TR = NT / R;
+  const int tid = threadIdx.x;
+  const int ii = tid / R, s = tid % R;
+  const int gr = blockIdx.x * TR + ii;
+  if (gr >= (int)G.rows) return;
+  const unsigned fl = flags[(long long)blockIdx.x * (NT / 32) + (tid >> 5)];
+  double2* cp = c + (long long)gr * G.L1 + s;
+  float2* dp = d ? d + (long long)gr * G.L1 + s : nullptr;
+#pragma unroll
+  for (int r = 0; r < KP; ++r)
+    if (!((fl >> r) & 1u)) {
+      cp[r * R] = make_double2(0.0, 0.0);
+      if (dp) dp[r * R] = make_float2(0.f, 0.f);
+    }
 }
 
 // Pass A for ADMM (complex128 engine).
@@ -706,7 +751,7 @@ struct ColsIO {
 
 // One line = (snapshot b, column k1): length L2, band K2.
 template <int KP, typename C>
-__global__ void __launch_bounds__(256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
+__global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int R = ax.R, K = ax.K, N = ax.N;

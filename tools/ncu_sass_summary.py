@@ -1,6 +1,7 @@
 """Summarise an ncu SASS source-page CSV: opcode mix, stall samples, hottest instructions.
 
-usage: ncu -i X.ncu-rep --page source --csv --print-source=sass > s.csv; python tools/ncu_sass_summary.py s.csv
+usage: ncu -i X.ncu-rep --page source --csv --print-source=sass > s.csv
+       python tools/ncu_sass_summary.py s.csv [kernel-name-substring]
 """
 import csv
 import sys
@@ -14,7 +15,8 @@ for r in rows:
         sections.append(cur)
     elif cur is not None:
         cur["rows"].append(r)
-for sec in sections[:1]:
+pick = [x for x in sections if len(sys.argv) < 3 or sys.argv[2] in x["name"]]
+for sec in pick[:1]:
     hdr = sec["rows"][0]
     data = [dict(zip(hdr, r)) for r in sec["rows"][1:] if len(r) == len(hdr)]
     num = lambda v: int(v) if v not in ("", "-") else 0  # noqa: E731
