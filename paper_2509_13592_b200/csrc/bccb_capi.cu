@@ -189,6 +189,8 @@ struct bccb_plan_s {
   int M = 0;                       // occupied elements (Gram plans)
   int* occ_dev = nullptr;          // [3][M]: m1, m2 (reduced mod L1 / L2), (m1 + m2) & 1
   int occ_alias = 0;               // some occupied cells alias (M1 > L1 or M2 > L2)
+  cudaStream_t aux = nullptr;      // second stream for the sub-batch split (created lazily)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool full() const { return ax1.K == L1 && ax2.K == L2; }
 };
 
@@ -274,6 +276,9 @@ static void free_plan(bccb_plan_s* p) {
   free_axis(p->ax2);
   cudaFree(p->lam_box_dev);
   cudaFree(p->occ_dev);
+  if (p->aux) cudaStreamDestroy(p->aux);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   cudaSetDevice(cur);
   delete p;
 }
@@ -968,6 +973,25 @@ static int check_singular_admm(const bccb_plan_s* p, double rho) {
   return BCCB_OK;
 }
 
+// Sub-batch split (BCCB_SUBSTREAMS=1 disables): only when each half still fills the GPU.
+static int sub_batches(const bccb_plan_s* p, int batch) {
+  static const int env = [] {
+    const char* e = getenv("BCCB_SUBSTREAMS");
+    return e ? atoi(e) : 2;
+  }();
+  if (env < 2 || batch < 2) return 1;
+  const long long half_lines = (long long)(batch / 2) * p->L2;
+  return half_lines >= 2048 ? 2 : 1;
+}
+
+static int ensure_aux_stream(bccb_plan_s* p) {
+  if (p->aux) return BCCB_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  return BCCB_OK;
+}
+
 extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int iterations,
                               double mu, const double* tau,
                               const void* bhat_box, const void* extra, void* c, void* d,
@@ -1005,28 +1029,72 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
       alpha = an;
     }
   }
-  e.it = first_iteration;
-  e.beta_cur = e.momentum ? beta[first_iteration] : 0.0;
-  e.beta_next = 0.0;
   // specialised shapes use zero-segment skipping: flags start all-ones (read everything) and
   // the skipped zeros are written back by one final pass
   const bool zs = fast_supported(p, batch, extra);
-  auto rows = [&](bool inv, bool fwd) {
-    return zs ? launch_rows_fista_fast(p, batch, inv, fwd, w, e, true, st)
-              : launch_rows_fista(p, batch, inv, fwd, w, e, st);
-  };
   if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes(p, batch), st));
-  if ((rc = rows(false, true))) return rc;
-  for (int t = first_iteration; t < t_end; ++t) {
-    if ((rc = launch_cols<float2>(p, batch, true, true, w, (const float2*)w.D, (const float2*)w.P,
-                                  (const float2*)bhat_box, nullptr, st)))
-      return rc;
-    e.it = t;
-    e.beta_cur = e.momentum ? beta[t] : 0.0;
-    e.beta_next = e.momentum ? beta[t + 1] : 0.0;
-    if ((rc = rows(true, t + 1 < t_end))) return rc;
+
+  // Sub-batch split: two halves of the batch run on two streams, so one half's (latency-bound)
+  // column pass and kernel tails overlap the other half's rows pass.  Snapshots are
+  // independent, so the arithmetic is identical to one stream (bitwise).
+  const int nsub = sub_batches(p, batch);
+  if (nsub > 1 && (rc = ensure_aux_stream(p))) return rc;
+  struct Sub {
+    int b0, nb;
+    cudaStream_t st;
+    Workspace w;
+    EpiFista e;
+  } sub[2];
+  for (int q = 0; q < nsub; ++q) {
+    Sub& u = sub[q];
+    u.b0 = (int)((long long)batch * q / nsub);
+    u.nb = (int)((long long)batch * (q + 1) / nsub) - u.b0;
+    u.st = q == 0 ? st : p->aux;
+    u.w = w;
+    const long long inter = (long long)u.b0 * p->ax1.K * p->L2;
+    u.w.U = (float2*)w.U + inter;
+    u.w.V = (float2*)w.V + inter;
+    if (zs) u.w.flags = w.flags + zs_flag_bytes(p, u.b0);
+    u.e = e;
+    const long long off = (long long)u.b0 * p->L1 * p->L2;
+    u.e.c = e.c + off;
+    u.e.d = e.d ? e.d + off : nullptr;
+    u.e.extra = e.extra ? e.extra + off : nullptr;
+    u.e.tau = e.tau + u.b0;
+    u.e.first_bad = e.first_bad + u.b0;
+    u.e.it = first_iteration;
+    u.e.beta_cur = u.e.momentum ? beta[first_iteration] : 0.0;
+    u.e.beta_next = 0.0;
   }
-  if (zs && (rc = launch_zero_segments(p, batch, w, (double2*)c, (float2*)d, st))) return rc;
+  const float2* bh = (const float2*)bhat_box;
+  auto rows = [&](Sub& u, bool inv, bool fwd) {
+    return zs ? launch_rows_fista_fast(p, u.nb, inv, fwd, u.w, u.e, true, u.st)
+              : launch_rows_fista(p, u.nb, inv, fwd, u.w, u.e, u.st);
+  };
+  if (nsub > 1) {
+    CUDA_TRY(cudaEventRecord(p->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+  }
+  for (int q = 0; q < nsub; ++q)
+    if ((rc = rows(sub[q], false, true))) return rc;
+  for (int t = first_iteration; t < t_end; ++t) {
+    for (int q = 0; q < nsub; ++q) {
+      Sub& u = sub[q];
+      if ((rc = launch_cols<float2>(p, u.nb, true, true, u.w, (const float2*)w.D, (const float2*)w.P,
+                                    bh + (long long)u.b0 * p->ax1.K * p->ax2.K, nullptr, u.st)))
+        return rc;
+      u.e.it = t;
+      u.e.beta_cur = u.e.momentum ? beta[t] : 0.0;
+      u.e.beta_next = u.e.momentum ? beta[t + 1] : 0.0;
+      if ((rc = rows(u, true, t + 1 < t_end))) return rc;
+    }
+  }
+  for (int q = 0; q < nsub; ++q)
+    if (zs && (rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].e.c, sub[q].e.d, sub[q].st))) return rc;
+  if (nsub > 1) {
+    CUDA_TRY(cudaEventRecord(p->ev_join, p->aux));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
+  }
   return BCCB_OK;
 }
 

@@ -459,6 +459,37 @@ __global__ void __launch_bounds__(256, 1) rows_fista_pipe_kernel(Geo G, AxisT<fl
 // the warp's lanes at register slot r may be nonzero.  Clear segments are not read (they are
 // exactly zero) and not written while they stay zero; a segment that is (or becomes) nonzero
 // is written whole.  zero_segments_kernel writes the skipped zeros back at the end of a run.
+struct FistaScalars {
+  double kap, a_id, bc;
+  int b, it;
+  int* first_bad;
+};
+
+// Full float64 update of one point (solvers.py:245-249, 131-145, 336-337): returns c_{t+1}
+// and d_{t+1} (FISTA).  Out of line to keep the unrolled kernel small: only points with a
+// nonzero state or with |g| near / above the threshold take it.
+template <bool MOM>
+__device__ __noinline__ double2 fista_point_slow(double2 cc, float2 dd, float2 g, const FistaScalars sc,
+                                                  float2* dnew) {
+  double xr = cc.x, xi = cc.y;
+  if (MOM) {
+    xr = __fma_rn(sc.bc, (double)dd.x, xr);
+    xi = __fma_rn(sc.bc, (double)dd.y, xi);
+  }
+  const double wr = __fma_rn(sc.a_id, xr, (double)g.x);
+  const double wi = __fma_rn(sc.a_id, xi, (double)g.y);
+  if (!isfinite(wr + wi)) atomicMin(sc.first_bad + sc.b, sc.it);
+  const double m2 = wr * wr + wi * wi;
+  double nr = 0.0, ni = 0.0;
+  if (!(m2 <= sc.kap * sc.kap)) {
+    const double f = 1.0 - sc.kap * rsqrt(m2);
+    nr = wr * f;
+    ni = wi * f;
+  }
+  if (MOM) *dnew = make_float2((float)(nr - cc.x), (float)(ni - cc.y));
+  return make_double2(nr, ni);
+}
+
 template <int KP, int R, int MO, bool MOM, bool ZS>
 __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
     rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags) {
@@ -488,6 +519,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
   const double a_id = epi.a, bc = epi.beta_cur;
   const float bn = (float)epi.beta_next;
+  const FistaScalars sc{kap, a_id, bc, b, epi.it, epi.first_bad};
   const int lane = tid & 31;
   unsigned* fw = ZS ? flags + ((long long)blockIdx.x * (NT / 32) + (tid >> 5)) : nullptr;
   const unsigned fl = ZS ? *fw : 0xffffffffu;
@@ -548,21 +580,9 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
           float2 dnew = make_float2(0.f, 0.f);
           bool nz = false;
           if (active && !(zero_state && fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
-            double xr = cc.x, xi = cc.y;
-            if (MOM) {
-              xr = __fma_rn(bc, (double)dd.x, xr);
-              xi = __fma_rn(bc, (double)dd.y, xi);
-            }
-            const double wr = __fma_rn(a_id, xr, (double)g.x);
-            const double wi = __fma_rn(a_id, xi, (double)g.y);
-            if (!isfinite(wr + wi)) atomicMin(epi.first_bad + b, epi.it);
-            const double m2 = wr * wr + wi * wi;
-            if (!(m2 <= kap * kap)) {
-              const double f = 1.0 - kap * rsqrt(m2);
-              nr = wr * f;
-              ni = wi * f;
-            }
-            if (MOM) dnew = make_float2((float)(nr - cc.x), (float)(ni - cc.y));
+            const double2 cn = fista_point_slow<MOM>(cc, dd, g, sc, &dnew);
+            nr = cn.x;
+            ni = cn.y;
             nz = true;   // state touched: value may be nonzero or may have changed
             if (!ZS) {
               cp[r * R] = make_double2(nr, ni);
