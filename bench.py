@@ -275,7 +275,8 @@ def main():
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json copy test)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    rows_bytes = B_ALG_ROWS[w.solver] * B * L
+    fused_cols = n_k[1] == 0
+    rows_bytes = (B_ALG_ROWS[w.solver] + (B_ALG_COLS if fused_cols else 0)) * B * L
     achieved = rows_bytes / (rows_ms / 1e3) / 1e9
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -290,10 +291,12 @@ def main():
         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
         "traffic": traffic, "peak_source": peak_src,
         "algorithmic_bytes_per_launch": rows_bytes,
-        "bytes_model": f"{B_ALG_ROWS[w.solver]} B/gpi x {B}x{L} gpi per launch (SURVEY 8(d) K4+K2 share)",
+        "bytes_model": (f"{B_ALG_ROWS[w.solver]}{' + 16 (fused K3)' if fused_cols else ''} B/gpi x {B}x{L} gpi "
+                        "per launch (SURVEY 8(d) K4+K2 share)"),
         "avg_launch_ms": rows_ms, "share_of_step": ms_k[0] / step_kernel_ms,
-        "cols_kernel": {"avg_launch_ms": cols_ms, "achieved": B_ALG_COLS * B * L / (cols_ms / 1e3) / 1e9,
-                        "share_of_step": ms_k[1] / step_kernel_ms},
+        "cols_kernel": ({"avg_launch_ms": cols_ms, "achieved": B_ALG_COLS * B * L / (cols_ms / 1e3) / 1e9,
+                         "share_of_step": ms_k[1] / step_kernel_ms} if n_k[1] else
+                        {"fused": "column pass runs inside the rows kernel (last CTA per snapshot)"}),
         "iteration": {"bytes_per_gpi": B_ALG[w.solver], "achieved": iter_achieved,
                       "frac": iter_achieved / hbm_peak, "frac_vs_8TBs_spec": iter_achieved / 8000.0},
     }

@@ -445,6 +445,7 @@ struct Workspace {
   void* D;
   void* P;
   unsigned char* flags;  // zero-segment flags of the streaming FISTA pass
+  int* counters;         // [batch] arrival counters of the fused column pass
 };
 
 // threads per CTA of the specialised FISTA rows pass (flags: one 32-bit word per warp)
@@ -464,7 +465,8 @@ static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) {
 static size_t ws_bytes(const bccb_plan_s* p, int batch) {
   const size_t inter = (size_t)batch * p->ax1.K * p->L2 * sizeof(double2);
   const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
-  return 2 * align_up(inter) + 2 * align_up(box) + align_up(zs_flag_bytes(p, batch));
+  return 2 * align_up(inter) + 2 * align_up(box) + align_up(zs_flag_bytes(p, batch)) +
+         align_up((size_t)batch * sizeof(int));
 }
 
 static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
@@ -481,6 +483,8 @@ static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   w.P = ptr;
   ptr += box;
   w.flags = (unsigned char*)ptr;
+  ptr += align_up(zs_flag_bytes(p, batch));
+  w.counters = (int*)ptr;
   return w;
 }
 
@@ -664,9 +668,60 @@ static LaunchShape fast_shape(const bccb_plan_s* p) {
   return sh;
 }
 
+// Fused column pass: enabled when one snapshot's column work (K1 x L2 points) is no more than
+// one rows CTA's work (TR x L1 points) and the shape has a fused specialisation.
+#define FUSED_SHAPES(X) \
+  X(16, 4, 1, 16)  /* config 1 */ \
+  X(32, 8, 1, 16)  /* config 2 */
+
+static bool fused_supported(const bccb_plan_s* p) {
+  static const int env = [] {
+    const char* e = getenv("BCCB_FUSE_COLS");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env) return false;
+  const AxisPrec& a = p->ax1.f;
+  const int tr = zs_threads(p->ax1) / a.R;
+  if ((long long)p->ax1.K * p->L2 > (long long)tr * p->L1) return false;
+  const AxisPrec& c = p->ax2.s;
+  const int trc = std::min(zs_threads(p->ax1) / c.R, p->ax1.K);
+  if (trc < 1 || p->ax1.K % trc != 0) return false;
+  const int key = fast_key(a);
+#define FUSED_KEY(KP_, R_, MO_, KP2_) \
+  if (key == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_) return true;
+  FUSED_SHAPES(FUSED_KEY)
+#undef FUSED_KEY
+  return false;
+}
+
+static FusedCols make_fused(const bccb_plan_s* p, int batch, const Workspace& w, const float2* D, const float2* P,
+                            const float2* Bh) {
+  FusedCols fc{};
+  const AxisPrec& c = p->ax2.s;
+  fc.ax = p->ax2.dev_s();
+  fc.io.U = (const float2*)w.U;
+  fc.io.V = (float2*)w.V;
+  fc.io.D = D;
+  fc.io.P = P;
+  fc.io.Bh = Bh;
+  fc.io.box_out = nullptr;
+  fc.io.K1 = p->ax1.K;
+  fc.G.L1 = p->L1;
+  fc.G.L2 = p->L2;
+  fc.G.rows = (long long)batch * p->ax1.K;
+  fc.G.do_fwd = 1;
+  fc.G.do_inv = 1;
+  fc.TRc = std::min(zs_threads(p->ax1) / c.R, p->ax1.K);
+  fc.G.TR = fc.TRc;
+  fc.counter = w.counters;
+  fc.cps = p->L2 / (zs_threads(p->ax1) / p->ax1.f.R);
+  fc.K1 = p->ax1.K;
+  return fc;
+}
+
 static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
-                                  const EpiFista& epi, bool zs, cudaStream_t st) {
-  const LaunchShape sh = fast_shape(p);
+                                  const EpiFista& epi, bool zs, cudaStream_t st, const FusedCols* fused = nullptr) {
+  LaunchShape sh = fast_shape(p);
   const Geo G = rows_geo(p, batch, sh, inv, fwd);
   RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
@@ -674,17 +729,33 @@ static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, boo
   const bool mom = epi.momentum != 0;
   unsigned* fl = (unsigned*)w.flags;
   const int key = fast_key(p->ax1.f);
+  if (fused && zs) {
+    const AxisPrec& c = p->ax2.s;
+    const int pitch2 = (c.R % 2 == 1) ? c.R : c.R + 1;
+    const size_t need = ((size_t)fused->TRc * (p->ax2.K + 1) + (size_t)fused->TRc * c.KP * pitch2) * sizeof(float2);
+    sh.smem = std::max(sh.smem, need);
+#define FUSED_CASE(KP_, R_, MO_, KP2_)                                                                     \
+  if (key == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_)                                                 \
+    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true, KP2_>, KIND_ROWS, grid, sh,  \
+                                     st, G, ax, io, epi, fl, *fused)                                       \
+               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true, KP2_>, KIND_ROWS, grid, sh, \
+                                     st, G, ax, io, epi, fl, *fused);
+    FUSED_SHAPES(FUSED_CASE)
+#undef FUSED_CASE
+    return fail(BCCB_ERR_UNSUPPORTED, "no fused specialisation for this line shape");
+  }
+  const FusedCols nofc{};
 #define FAST_CASE(KP_, R_, MO_)                                                                              \
   if (key == KP_ * 100000 + R_ * 10 + MO_) {                                                                 \
     if (zs)                                                                                                  \
       return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true>, KIND_ROWS, grid, sh, st, \
-                                       G, ax, io, epi, fl)                                                   \
+                                       G, ax, io, epi, fl, nofc)                                             \
                  : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true>, KIND_ROWS, grid, sh,   \
-                                       st, G, ax, io, epi, fl);                                              \
+                                       st, G, ax, io, epi, fl, nofc);                                        \
     return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, false>, KIND_ROWS, grid, sh, st,  \
-                                     G, ax, io, epi, fl)                                                     \
+                                     G, ax, io, epi, fl, nofc)                                               \
                : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, false>, KIND_ROWS, grid, sh, st, \
-                                     G, ax, io, epi, fl);                                                    \
+                                     G, ax, io, epi, fl, nofc);                                              \
   }
   FAST_SHAPES(FAST_CASE)
 #undef FAST_CASE
@@ -1067,8 +1138,18 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
     u.e.beta_next = 0.0;
   }
   const float2* bh = (const float2*)bhat_box;
-  auto rows = [&](Sub& u, bool inv, bool fwd) {
-    return zs ? launch_rows_fista_fast(p, u.nb, inv, fwd, u.w, u.e, true, u.st)
+  const bool fuse = zs && fused_supported(p);
+  FusedCols fcs[2];
+  for (int q = 0; q < nsub && fuse; ++q)
+    fcs[q] = make_fused(p, sub[q].nb, sub[q].w, (const float2*)w.D, (const float2*)w.P,
+                        bh + (long long)sub[q].b0 * p->ax1.K * p->ax2.K);
+  if (fuse) {
+    for (int q = 0; q < nsub; ++q) fcs[q].counter = w.counters + sub[q].b0;
+    CUDA_TRY(cudaMemsetAsync(w.counters, 0, (size_t)batch * sizeof(int), st));
+  }
+  auto rows = [&](int q, bool inv, bool fwd) {
+    Sub& u = sub[q];
+    return zs ? launch_rows_fista_fast(p, u.nb, inv, fwd, u.w, u.e, true, u.st, fuse ? &fcs[q] : nullptr)
               : launch_rows_fista(p, u.nb, inv, fwd, u.w, u.e, u.st);
   };
   if (nsub > 1) {
@@ -1076,17 +1157,18 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
     CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
   }
   for (int q = 0; q < nsub; ++q)
-    if ((rc = rows(sub[q], false, true))) return rc;
+    if ((rc = rows(q, false, true))) return rc;
   for (int t = first_iteration; t < t_end; ++t) {
     for (int q = 0; q < nsub; ++q) {
       Sub& u = sub[q];
-      if ((rc = launch_cols<float2>(p, u.nb, true, true, u.w, (const float2*)w.D, (const float2*)w.P,
+      if (!fuse &&
+          (rc = launch_cols<float2>(p, u.nb, true, true, u.w, (const float2*)w.D, (const float2*)w.P,
                                     bh + (long long)u.b0 * p->ax1.K * p->ax2.K, nullptr, u.st)))
         return rc;
       u.e.it = t;
       u.e.beta_cur = u.e.momentum ? beta[t] : 0.0;
       u.e.beta_next = u.e.momentum ? beta[t + 1] : 0.0;
-      if ((rc = rows(u, true, t + 1 < t_end))) return rc;
+      if ((rc = rows(q, true, t + 1 < t_end))) return rc;
     }
   }
   for (int q = 0; q < nsub; ++q)

@@ -215,6 +215,85 @@ __device__ __forceinline__ void rows_forward_store(const Geo& G, const AxisT<C>&
   }
 }
 
+// ------------------------------------------------------------------ pass B
+template <typename C>
+struct ColsIO {
+  const C* __restrict__ U;          // [B][K1][L2] forward input (do_fwd)
+  C* __restrict__ V;                // [B][K1][L2] inverse output (do_inv)
+  const C* __restrict__ D;          // [K1][K2] multiplier (null => identity)
+  const C* __restrict__ P;          // [K1][K2] rhs multiplier (null => 1)
+  const float2* __restrict__ Bh;    // [B][K1][K2] rhs box, complex64 data (null => none)
+  C* __restrict__ box_out;          // [B][K1][K2] (used when !do_inv)
+  int K1;
+};
+
+// Column lines [row0, row0 + TR) (line = (snapshot b, column k1): length L2, band K2) processed
+// by one CTA of TR * ax.R threads (threads beyond that idle).  Shared by cols_kernel and the
+// fused rows kernel.  smem: TR x (K+1) band tile + TR x KP x pitch transpose buffer.
+template <int KP, typename C>
+__device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, const ColsIO<C>& io, long long row0,
+                                           int TR, C* smem) {
+  const int R = ax.R, K = ax.K, N = ax.N;
+  const int XP = K + 1, SP = KP * ax.pitch;
+  const int nthr = TR * R;
+  const int tid = threadIdx.x;
+  const int ii = tid / R, s = tid - ii * R;
+  const long long gr = row0 + ii;
+  const bool active = (tid < nthr) && (gr < G.rows);
+  C* Xs = smem;
+  C* S = smem + TR * XP;
+  C a[KP];
+  if (G.do_fwd) {
+    if (active) {
+      const C* line = io.U + gr * N + s;
+#pragma unroll
+      for (int r = 0; r < KP; ++r) a[r] = __ldcg(line + (long long)R * r);  // L2: written this launch
+      reg_dft<KP, false>(a);
+      band_fwd_scatter<KP>(a, s, ax, S + ii * SP);
+    }
+    __syncthreads();
+  }
+  // band values: Y = D*X + P*Bh
+  for (int idx = tid; idx < TR * K; idx += blockDim.x) {
+    const int i2 = idx / K, o = idx - i2 * K;
+    const long long g2 = row0 + i2;
+    if (g2 >= G.rows) continue;
+    const long long k1 = g2 % io.K1;
+    C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
+    if (G.do_fwd) {
+      y = band_fwd_output(S + i2 * SP, o, KP, ax);
+      if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
+    }
+    if (io.Bh) {
+      C bh = to_c(io.Bh[g2 * K + o], C{});
+      if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
+      y = cadd(y, bh);
+    }
+    Xs[i2 * XP + o] = y;
+  }
+  __syncthreads();
+  if (G.do_inv) {
+    if (active) {
+      band_inverse<KP>(Xs + ii * XP, s, ax, a);
+      C* line = io.V + gr * N + s;
+#pragma unroll
+      for (int r = 0; r < KP; ++r) line[(long long)R * r] = a[r];
+    }
+  } else {
+    for (int idx = tid; idx < TR * K; idx += blockDim.x) {
+      const int i2 = idx / K, o = idx - i2 * K;
+      const long long g2 = row0 + i2;
+      if (g2 < G.rows) io.box_out[g2 * K + o] = Xs[i2 * XP + o];
+    }
+  }
+}
+
+template <int KP, typename C>
+__global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cols_block<KP>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR, reinterpret_cast<C*>(smem_raw));
+}
+
 // ------------------------------------------------------------------ pass A kernels
 // Generic pass A for plain-vector epilogues.
 template <int KP, typename C>
@@ -490,9 +569,24 @@ __device__ __noinline__ double2 fista_point_slow(double2 cc, float2 dd, float2 g
   return make_double2(nr, ni);
 }
 
-template <int KP, int R, int MO, bool MOM, bool ZS>
+// Fused column pass (KP2 > 0): the column work of one snapshot (K1 lines of length L2) is at
+// most one CTA's rows work for small grids (config 2: 32 x 256 vs 32 x 256 points), so the last
+// rows CTA to finish a snapshot (threadfence + atomic counter) runs that snapshot's column
+// lines in place, overlapping other snapshots' rows work and halving the launches.
+struct FusedCols {
+  ColsIO<float2> io;
+  AxisT<float2> ax;
+  Geo G;          // column-line geometry (rows = B * K1)
+  int* counter;   // [B] arrival counters (monotonic; last arrival when count % cps == 0)
+  int cps;        // rows CTAs per snapshot
+  int TRc;        // column lines per block pass (divides K1)
+  int K1;
+};
+
+template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0>
 __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
-    rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags) {
+    rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
+                           FusedCols fc) {
   constexpr int NT = R > 256 ? R : 256;   // threads per CTA
   constexpr int TR = NT / R;
   constexpr int K = KP * MO;
@@ -630,8 +724,21 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
     }
   }
   if (!G.do_fwd) return;
-  // ---- band forward: register DFT, twiddle + transpose scatter, R-term reductions
-  if (active) {
+  // ---- band forward: register DFT, twiddle + transpose scatter, R-term reductions.
+  // A line whose next operator input is entirely zero (most lines once the iterate is sparse)
+  // has a zero band: its DFT, scatter and reductions are skipped.
+  __shared__ unsigned live_rows[(TR + 31) / 32];
+  if (tid < (TR + 31) / 32) live_rows[tid] = 0u;
+  __syncthreads();
+  {
+    bool nzx = false;
+#pragma unroll
+    for (int r = 0; r < KP; ++r) nzx |= (a[r].x != 0.f) | (a[r].y != 0.f);
+    if (active && nzx) atomicOr(&live_rows[ii >> 5], 1u << (ii & 31));
+  }
+  __syncthreads();
+  const bool my_live = (live_rows[ii >> 5] >> (ii & 31)) & 1u;
+  if (active && my_live) {
     reg_dft<KP, false>(a);
     float2* Srow = S + ii * SP;
 #pragma unroll
@@ -640,6 +747,10 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   __syncthreads();
   for (int idx = tid; idx < TR * K; idx += NT) {
     const int i2 = idx / K, o = idx % K;
+    if (!((live_rows[i2 >> 5] >> (i2 & 31)) & 1u)) {
+      Xs[i2 * XP + o] = make_float2(0.f, 0.f);
+      continue;
+    }
     const int j = o % KP, m = o / KP;
     const float2* row = S + i2 * SP + j * PITCH;
     float2 acc = make_float2(0.f, 0.f);
@@ -657,6 +768,18 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   for (int idx = tid; idx < TR * K; idx += NT) {
     const int k = idx / TR, i2 = idx % TR;
     if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
+  }
+  if constexpr (KP2 > 0) {
+    __shared__ int s_last;
+    __threadfence();                       // publish this CTA's U tile
+    __syncthreads();
+    if (tid == 0) s_last = ((atomicAdd(fc.counter + b, 1) + 1) % fc.cps) == 0;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();                     // acquire the other CTAs' U tiles
+      for (int l0 = 0; l0 < fc.K1; l0 += fc.TRc)
+        cols_block<KP2>(fc.G, fc.ax, fc.io, (long long)b * fc.K1 + l0, fc.TRc, Xs);
+    }
   }
 }
 
@@ -754,77 +877,6 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, AxisT<double2> ax
   if (G.do_fwd) {
     if (G.do_inv) __syncthreads();
     rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
-  }
-}
-
-// ------------------------------------------------------------------ pass B
-template <typename C>
-struct ColsIO {
-  const C* __restrict__ U;          // [B][K1][L2] forward input (do_fwd)
-  C* __restrict__ V;                // [B][K1][L2] inverse output (do_inv)
-  const C* __restrict__ D;          // [K1][K2] multiplier (null => identity)
-  const C* __restrict__ P;          // [K1][K2] rhs multiplier (null => 1)
-  const float2* __restrict__ Bh;    // [B][K1][K2] rhs box, complex64 data (null => none)
-  C* __restrict__ box_out;          // [B][K1][K2] (used when !do_inv)
-  int K1;
-};
-
-// One line = (snapshot b, column k1): length L2, band K2.
-template <int KP, typename C>
-__global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* smem = reinterpret_cast<C*>(smem_raw);
-  const int R = ax.R, K = ax.K, N = ax.N;
-  const int TR = G.TR, XP = K + 1, SP = KP * ax.pitch;
-  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
-  const long long row0 = (long long)blockIdx.x * TR;
-  const long long gr = row0 + ii;
-  const bool active = (ii < TR) && (gr < G.rows);
-  C* Xs = smem;
-  C* S = smem + TR * XP;
-  C a[KP];
-  if (G.do_fwd) {
-    if (active) {
-      const C* line = io.U + gr * N + s;
-#pragma unroll
-      for (int r = 0; r < KP; ++r) a[r] = line[(long long)R * r];
-      reg_dft<KP, false>(a);
-      band_fwd_scatter<KP>(a, s, ax, S + ii * SP);
-    }
-    __syncthreads();
-  }
-  // band values: Y = D*X + P*Bh
-  for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
-    const int i2 = idx / K, o = idx - i2 * K;
-    const long long g2 = row0 + i2;
-    if (g2 >= G.rows) continue;
-    const long long k1 = g2 % io.K1;
-    C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
-    if (G.do_fwd) {
-      y = band_fwd_output(S + i2 * SP, o, KP, ax);
-      if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
-    }
-    if (io.Bh) {
-      C bh = to_c(io.Bh[g2 * K + o], C{});
-      if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
-      y = cadd(y, bh);
-    }
-    Xs[i2 * XP + o] = y;
-  }
-  __syncthreads();
-  if (G.do_inv) {
-    if (active) {
-      band_inverse<KP>(Xs + ii * XP, s, ax, a);
-      C* line = io.V + gr * N + s;
-#pragma unroll
-      for (int r = 0; r < KP; ++r) line[(long long)R * r] = a[r];
-    }
-  } else {
-    for (int idx = threadIdx.x; idx < TR * K; idx += blockDim.x) {
-      const int i2 = idx / K, o = idx - i2 * K;
-      const long long g2 = row0 + i2;
-      if (g2 < G.rows) io.box_out[g2 * K + o] = Xs[i2 * XP + o];
-    }
   }
 }
 

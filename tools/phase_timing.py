@@ -32,3 +32,16 @@ for rep in range(2):
         nnz = float((c != 0).float().mean())
         out.append((a, b2, round(e0.elapsed_time(e1) * 1e3 / (b2 - a), 2), round(nnz, 5)))
 print(json.dumps({"cfg": cfg, "phases [a,b,us_per_iter,c_density]": out}))
+# device time of the kernels alone over a late window (launch gaps = event time - kernel sum)
+import ctypes
+c.zero_(); d.zero_(); run(0, 400)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); run(400, 100); e1.record(); e1.synchronize()
+ev_us = e0.elapsed_time(e1) * 1e3 / 100
+_lib.lib.bccb_profile_begin(); run(400, 100)
+ms = (ctypes.c_double * 3)(); n = (ctypes.c_longlong * 3)()
+_lib.check(_lib.lib.bccb_profile_end(ms, n))
+print(json.dumps({"cfg": cfg, "late_event_us_per_iter": round(ev_us, 2), "rows_us": round(ms[0] * 1e3 / max(n[0], 1), 2),
+                  "cols_us": round(ms[1] * 1e3 / max(n[1], 1), 2), "cols_launches": n[1],
+                  "kernel_sum_us_per_iter": round((ms[0] + ms[1]) * 1e3 / 100, 2)}))
