@@ -667,6 +667,12 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
         for (int q = 0; q < CH; ++q) {
           const int r = r0 + q;
           const float2 g = a[r];
+          // Warp-level fast path: a clear segment whose 32 points all stay below the threshold
+          // stays exactly zero (same test as the per-point fast path below).
+          if (ZS && !((fl >> r) & 1u) && __all_sync(0xffffffffu, fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
+            a[r] = make_float2(0.f, 0.f);
+            continue;
+          }
           const double2 cc = cb[q];
           const float2 dd = db[q];
           const bool zero_state = (cc.x == 0.0) & (cc.y == 0.0) & (!MOM | ((dd.x == 0.f) & (dd.y == 0.f)));

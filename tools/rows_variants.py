@@ -30,7 +30,7 @@ _lib.lib.bccb_profile_begin()
 run()
 ms = (ctypes.c_double * 3)(); n = (ctypes.c_longlong * 3)()
 _lib.check(_lib.lib.bccb_profile_end(ms, n))
-rows = ms[0] / n[0]; cols = ms[1] / n[1]
+rows = ms[0] / max(n[0], 1); cols = ms[1] / max(n[1], 1)
 gbs = 48 * B * L / (rows / 1e3) / 1e9
 print(json.dumps({"cfg": cfg, "variant": os.environ.get("BCCB_ROWS_VARIANT", "1"), "rows_ms": round(rows, 4),
                   "cols_ms": round(cols, 4), "rows_actual_GBs": round(gbs), "iter_ms": round((ms[0] + ms[1]) / T, 4)}))
