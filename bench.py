@@ -258,15 +258,18 @@ def main():
     gpi_step = B * L * T
     value = world * gpi_step / (ms_step / 1e3)
 
-    # ---- per-kernel live timing (one extra profiled step, events around every launch)
+    # ---- per-kernel live timing: one extra profiled step, single stream (one launch = the whole
+    # batch, no concurrent-stream overlap inside the event brackets), events around every launch
     reset()
     torch.cuda.synchronize(dev)
+    _lib.check(_lib.lib.bccb_set_substreams(1))
     _lib.lib.bccb_profile_begin()
     run()
     import ctypes
     ms_k = (ctypes.c_double * 3)()
     n_k = (ctypes.c_longlong * 3)()
     _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
+    _lib.check(_lib.lib.bccb_set_substreams(2))
     rows_ms = ms_k[0] / max(n_k[0], 1)
     cols_ms = ms_k[1] / max(n_k[1], 1)
     step_kernel_ms = ms_k[0] + ms_k[1] + ms_k[2]
@@ -282,18 +285,21 @@ def main():
     ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(ncu_path):
         try:
-            traffic = json.load(open(ncu_path)).get(f"cfg{w.cfg}", {}).get("rows_dram_bytes_per_launch")
+            per_gpi = json.load(open(ncu_path)).get(f"cfg{w.cfg}", {}).get("rows_dram_bytes_per_gpi")
+            traffic = None if per_gpi is None else per_gpi * B * L   # DRAM bytes per (full-batch) launch
         except Exception:
             traffic = None
     iter_achieved = B_ALG[w.solver] * (value / world) / 1e9
     roofline = {
         "bound": "hbm", "kernel": f"rows_{w.solver}_kernel (band IFFT + fused epilogue + band FFT)",
         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-        "traffic": traffic, "peak_source": peak_src,
+        "traffic": traffic, "traffic_source": "profiles/ncu_summary.json (ncu dram__bytes_read+write, solve average)",
+        "peak_source": peak_src,
         "algorithmic_bytes_per_launch": rows_bytes,
         "bytes_model": (f"{B_ALG_ROWS[w.solver]}{' + 16 (fused K3)' if fused_cols else ''} B/gpi x {B}x{L} gpi "
                         "per launch (SURVEY 8(d) K4+K2 share)"),
         "avg_launch_ms": rows_ms, "share_of_step": ms_k[0] / step_kernel_ms,
+        "launch_timing": "profiled extra step, single stream, CUDA events on the launch stream",
         "cols_kernel": ({"avg_launch_ms": cols_ms, "achieved": B_ALG_COLS * B * L / (cols_ms / 1e3) / 1e9,
                          "share_of_step": ms_k[1] / step_kernel_ms} if n_k[1] else
                         {"fused": "column pass runs inside the rows kernel (last CTA per snapshot)"}),

@@ -49,6 +49,7 @@ SIGNATURES = {
     "bccb_launch_count": (_ll, []),
     "bccb_profile_begin": (_i, []),
     "bccb_profile_end": (_i, [_vp, _vp]),
+    "bccb_set_substreams": (_i, [_i]),
 }
 
 

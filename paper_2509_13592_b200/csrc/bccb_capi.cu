@@ -454,18 +454,25 @@ static size_t zs_flag_bytes(const bccb_plan_s* p, int batch);
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) {
-  const int nt = zs_threads(p->ax1);
-  const int tr = nt / p->ax1.f.R;
+static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R) {
+  const int nt = std::max(256, R);
+  const int tr = nt / R;
   const long long rows = (long long)batch * p->L2;
   const long long ctas = (rows + tr - 1) / tr;
   return (size_t)ctas * (nt / 32) * sizeof(unsigned);
 }
 
+// flags of the specialised FISTA rows pass (complex64 axis)
+static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, p->ax1.f.R); }
+
+// flags of the specialised ADMM rows pass (complex128 axis)
+static size_t zs_flag_bytes_d(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, p->ax1.d.R); }
+
 static size_t ws_bytes(const bccb_plan_s* p, int batch) {
   const size_t inter = (size_t)batch * p->ax1.K * p->L2 * sizeof(double2);
   const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
-  return 2 * align_up(inter) + 2 * align_up(box) + align_up(zs_flag_bytes(p, batch)) +
+  return 2 * align_up(inter) + 2 * align_up(box) +
+         align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch))) +
          align_up((size_t)batch * sizeof(int));
 }
 
@@ -483,7 +490,7 @@ static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   w.P = ptr;
   ptr += box;
   w.flags = (unsigned char*)ptr;
-  ptr += align_up(zs_flag_bytes(p, batch));
+  ptr += align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch)));
   w.counters = (int*)ptr;
   return w;
 }
@@ -760,6 +767,70 @@ static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, boo
   FAST_SHAPES(FAST_CASE)
 #undef FAST_CASE
   return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
+}
+
+// Specialised line shapes of the ADMM rows pass (complex128 axis, KP <= 16).
+#define ADMM_SHAPES(X)                                   \
+  X(16, 4, 1)    /* L1 = 64,   band 16 */                \
+  X(16, 16, 2)   /* L1 = 256,  band 32 */                \
+  X(16, 32, 4)   /* L1 = 512,  band 64  (config 3) */    \
+  X(16, 64, 4)   /* L1 = 1024, band 64 */                \
+  X(16, 256, 8)  /* L1 = 4096, band 128 */
+
+static bool admm_fast_supported(const bccb_plan_s* p, int batch, const void* extra) {
+  if (extra || rows_variant() != 0) return false;
+  const AxisPrec& a = p->ax1.d;
+  const int tr = std::max(256, a.R) / a.R;
+  if ((long long)batch * p->L2 >= (1LL << 31) || p->L2 % tr != 0) return false;
+  const int key = fast_key(a);
+#define ADMM_KEY(KP_, R_, MO_) \
+  if (key == KP_ * 100000 + R_ * 10 + MO_) return true;
+  ADMM_SHAPES(ADMM_KEY)
+#undef ADMM_KEY
+  return false;
+}
+
+static LaunchShape admm_shape(const bccb_plan_s* p) {
+  const AxisPrec& a = p->ax1.d;
+  LaunchShape sh;
+  sh.threads = std::max(256, a.R);
+  sh.TR = sh.threads / a.R;
+  const int pitch = (a.R % 2 == 1) ? a.R : a.R + 1;
+  sh.smem = ((size_t)sh.TR * (p->ax1.K + 1) + (size_t)sh.TR * a.KP * pitch) * sizeof(double2);
+  return sh;
+}
+
+static int launch_rows_admm_fast(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
+                                 const EpiAdmm& epi, cudaStream_t st) {
+  const LaunchShape sh = admm_shape(p);
+  const Geo G = rows_geo(p, batch, sh, inv, fwd);
+  RowsIO<double2> io{(const double2*)w.V, (double2*)w.U};
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const AxisT<double2> ax = p->ax1.dev<double2>();
+  unsigned* fl = (unsigned*)w.flags;
+  const int key = fast_key(p->ax1.d);
+#define ADMM_CASE(KP_, R_, MO_)                                                                          \
+  if (key == KP_ * 100000 + R_ * 10 + MO_)                                                               \
+    return launch_pass<double2>(rows_admm_fast_kernel<KP_, R_, MO_, true>, KIND_ROWS, grid, sh, st, G, ax, io, \
+                                epi, fl);
+  ADMM_SHAPES(ADMM_CASE)
+#undef ADMM_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no ADMM specialisation for this line shape");
+}
+
+static int launch_zero_segments_z(const bccb_plan_s* p, int batch, const Workspace& w, float2* z, cudaStream_t st) {
+  LaunchShape sh = admm_shape(p);
+  const Geo G = rows_geo(p, batch, sh, false, false);
+  sh.smem = 0;
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const int key = fast_key(p->ax1.d);
+  const unsigned* fl = (const unsigned*)w.flags;
+#define ZZ_CASE(KP_, R_, MO_)                                                                             \
+  if (key == KP_ * 100000 + R_ * 10 + MO_)                                                                \
+    return launch_pass<double2>(zero_segments_z_kernel<KP_, R_>, KIND_OTHER, grid, sh, st, G, z, fl);
+  ADMM_SHAPES(ZZ_CASE)
+#undef ZZ_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no ADMM specialisation for this line shape");
 }
 
 static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace& w, double2* c, float2* d,
@@ -1044,12 +1115,22 @@ static int check_singular_admm(const bccb_plan_s* p, double rho) {
   return BCCB_OK;
 }
 
-// Sub-batch split (BCCB_SUBSTREAMS=1 disables): only when each half still fills the GPU.
+// Sub-batch split (BCCB_SUBSTREAMS=1 or bccb_set_substreams(1) disables): only when each half
+// still fills the GPU.
+static std::atomic<int> g_substreams{-1};
+
+extern "C" int bccb_set_substreams(int n) {
+  if (n < 1 || n > 2) return fail(BCCB_ERR_INVALID, "substreams must be 1 or 2");
+  g_substreams.store(n);
+  return BCCB_OK;
+}
+
 static int sub_batches(const bccb_plan_s* p, int batch) {
-  static const int env = [] {
+  int env = g_substreams.load();
+  if (env < 0) {
     const char* e = getenv("BCCB_SUBSTREAMS");
-    return e ? atoi(e) : 2;
-  }();
+    env = e ? atoi(e) : 2;
+  }
   if (env < 2 || batch < 2) return 1;
   const long long half_lines = (long long)(batch / 2) * p->L2;
   return half_lines >= 2048 ? 2 : 1;
@@ -1210,15 +1291,22 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
   e.extra_scale = 1.0 / (lo + rho);
   e.it = first_iteration;
   const int t_end = first_iteration + iterations;
-  if ((rc = launch_rows_admm(p, batch, false, true, w, e, st))) return rc;
+  // specialised shapes: zero-segment skipping on the sparse z (dual v is dense)
+  const bool zs = admm_fast_supported(p, batch, extra);
+  if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes_d(p, batch), st));
+  auto rows = [&](bool inv, bool fwd) {
+    return zs ? launch_rows_admm_fast(p, batch, inv, fwd, w, e, st) : launch_rows_admm(p, batch, inv, fwd, w, e, st);
+  };
+  if ((rc = rows(false, true))) return rc;
   for (int t = first_iteration; t < t_end; ++t) {
     if ((rc = launch_cols<double2>(p, batch, true, true, w, (const double2*)w.D, (const double2*)w.P,
                                    (const float2*)bhat_box, nullptr, st)))
       return rc;
     e.it = t;
     e.c_out = (t + 1 == t_end) ? (double2*)c_last : nullptr;
-    if ((rc = launch_rows_admm(p, batch, true, t + 1 < t_end, w, e, st))) return rc;
+    if ((rc = rows(true, t + 1 < t_end))) return rc;
   }
+  if (zs && (rc = launch_zero_segments_z(p, batch, w, (float2*)z, st))) return rc;
   return BCCB_OK;
 }
 

@@ -789,6 +789,165 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   }
 }
 
+// ---------------------------------------------------------------- specialised pass A (ADMM)
+// Complex128 engine, compile-time line shape (KP <= 16, R, MO).  State: z (complex64, sparse:
+// zero-segment flags as in the FISTA kernel) and the scaled dual v (complex128, dense, always
+// streamed).  Per point (solvers.py:426-430): u = z - v; c = a*u + g (+ q folded in g);
+// z' = S_{rho tau}(c + v); v' = v + (c - z'); next operator input u' = z' - v'.
+template <int KP, int R, int MO, bool ZS>
+__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
+    rows_admm_fast_kernel(Geo G, AxisT<double2> ax, RowsIO<double2> io, EpiAdmm epi, unsigned* __restrict__ flags) {
+  constexpr int NT = R > 256 ? R : 256;
+  constexpr int TR = NT / R;
+  constexpr int K = KP * MO;
+  constexpr int XP = K + 1;
+  constexpr int PITCH = (R % 2 == 1) ? R : R + 1;
+  constexpr int SP = KP * PITCH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Xs = reinterpret_cast<double2*>(smem_raw);
+  double2* S = Xs + TR * XP;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int ii = tid / R, s = tid % R;
+  const int row0 = blockIdx.x * TR;
+  const int gr = row0 + ii;
+  const bool active = gr < (int)G.rows;
+  const int L2 = G.L2;
+  const int b = row0 / L2;
+  const int l20 = row0 - b * L2;
+  const long long vbase = (long long)b * K * L2 + l20;
+  float2* zp = epi.z + (long long)gr * G.L1 + s;
+  double2* vp = epi.v + (long long)gr * G.L1 + s;
+  double2* cop = epi.c_out ? epi.c_out + (long long)gr * G.L1 + s : nullptr;
+  const double kap = epi.kscale * epi.tau[b];
+  const double kap2 = kap * kap;
+  const double a_id = epi.a;
+  unsigned* fw = ZS ? flags + ((long long)blockIdx.x * (NT / 32) + (tid >> 5)) : nullptr;
+  const unsigned fl = ZS ? *fw : 0xffffffffu;
+  double2 a[KP];
+
+  if (G.do_inv) {
+    for (int idx = tid; idx < TR * K; idx += NT) {
+      const int k = idx / TR, i2 = idx % TR;
+      Xs[i2 * XP + k] = io.V[vbase + (long long)k * L2 + i2];
+    }
+    float2 z0 = make_float2(0.f, 0.f), z1 = z0;
+    double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+    if (active) {
+      if (fl & 1u) z0 = zp[0];
+      if ((fl >> 1) & 1u) z1 = zp[R];
+      v0 = vp[0];
+      v1 = vp[R];
+    }
+    __syncthreads();
+    {
+      const double2* Y = Xs + ii * XP;
+#pragma unroll
+      for (int j = 0; j < KP; ++j) a[j] = Y[j];
+#pragma unroll
+      for (int m = 1; m < MO; ++m) {
+        const double2 w2 = __ldg(ax.tw2 + m * R + s);
+#pragma unroll
+        for (int j = 0; j < KP; ++j) a[j] = cadd(a[j], cmulc(Y[j + KP * m], w2));
+      }
+#pragma unroll
+      for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], __ldg(ax.tw1 + j * R + s));
+      reg_dft<KP, true>(a);
+    }
+    unsigned nfl = 0;
+#pragma unroll
+    for (int r = 0; r < KP; ++r) {
+      const float2 zz = z0;
+      const double2 vv = v0;
+      z0 = z1;
+      v0 = v1;
+      if (r + 2 < KP && active) {
+        z1 = ((fl >> (r + 2)) & 1u) ? zp[(r + 2) * R] : make_float2(0.f, 0.f);
+        v1 = vp[(r + 2) * R];
+      }
+      const double2 g = a[r];
+      const double cr = __fma_rn(a_id, (double)zz.x - vv.x, g.x);
+      const double ci = __fma_rn(a_id, (double)zz.y - vv.y, g.y);
+      if (active && !isfinite(cr + ci)) atomicMin(epi.first_bad + b, epi.it);
+      const double sr = cr + vv.x, si = ci + vv.y;
+      const double m2 = sr * sr + si * si;
+      float2 zn = make_float2(0.f, 0.f);
+      if (!(m2 <= kap2)) {
+        const double f = 1.0 - kap * rsqrt(m2);
+        zn = make_float2((float)(sr * f), (float)(si * f));
+      }
+      // v' = v + (c - z') on the stored z (bitwise identity of test_solvers.py:283-295)
+      const double2 vn = make_double2(vv.x + (cr - (double)zn.x), vv.y + (ci - (double)zn.y));
+      if (active) {
+        vp[r * R] = vn;
+        if (cop) cop[r * R] = make_double2(cr, ci);
+      }
+      if (ZS) {
+        const bool nzv = (zn.x != 0.f) | (zn.y != 0.f);
+        if (__any_sync(0xffffffffu, nzv)) {
+          if (active) zp[r * R] = zn;
+          nfl |= 1u << r;
+        }
+      } else if (active) {
+        zp[r * R] = zn;
+      }
+      a[r] = make_double2((double)zn.x - vn.x, (double)zn.y - vn.y);
+    }
+    if (ZS && lane == 0) *fw = nfl;
+  } else if (active) {
+#pragma unroll
+    for (int r = 0; r < KP; ++r) {
+      const float2 zz = ((fl >> r) & 1u) ? zp[r * R] : make_float2(0.f, 0.f);
+      const double2 vv = vp[r * R];
+      a[r] = make_double2((double)zz.x - vv.x, (double)zz.y - vv.y);
+    }
+  }
+  if (!G.do_fwd) return;
+  if (active) {
+    reg_dft<KP, false>(a);
+    double2* Srow = S + ii * SP;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], __ldg(ax.tw1 + j * R + s));
+  }
+  __syncthreads();
+  for (int idx = tid; idx < TR * K; idx += NT) {
+    const int i2 = idx / K, o = idx % K;
+    const int j = o % KP, m = o / KP;
+    const double2* row = S + i2 * SP + j * PITCH;
+    double2 acc = make_double2(0.0, 0.0);
+    if (m == 0) {
+#pragma unroll 8
+      for (int t = 0; t < R; ++t) acc = cadd(acc, row[t]);
+    } else {
+      const double2* tw = ax.tw2 + m * R;
+#pragma unroll 8
+      for (int t = 0; t < R; ++t) acc = cfma(row[t], __ldg(tw + t), acc);
+    }
+    Xs[i2 * XP + o] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < TR * K; idx += NT) {
+    const int k = idx / TR, i2 = idx % TR;
+    if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
+  }
+}
+
+// Final zero pass for z of a zero-skipping ADMM run.
+template <int KP, int R>
+__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_z_kernel(Geo G, float2* z,
+                                                                            const unsigned* __restrict__ flags) {
+  constexpr int NT = R > 256 ? R : 256;
+  constexpr int TR = NT / R;
+  const int tid = threadIdx.x;
+  const int ii = tid / R, s = tid % R;
+  const int gr = blockIdx.x * TR + ii;
+  if (gr >= (int)G.rows) return;
+  const unsigned fl = flags[(long long)blockIdx.x * (NT / 32) + (tid >> 5)];
+  float2* zp = z + (long long)gr * G.L1 + s;
+#pragma unroll
+  for (int r = 0; r < KP; ++r)
+    if (!((fl >> r) & 1u)) zp[r * R] = make_float2(0.f, 0.f);
+}
+
 // Final pass of a zero-skipping run: write the zeros of every clear segment back so c (and d)
 // are dense, consistent arrays again.
 template <int KP, int R>
