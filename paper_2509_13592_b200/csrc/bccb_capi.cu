@@ -190,6 +190,9 @@ struct bccb_plan_s {
   int* occ_dev = nullptr;          // [3][M]: m1, m2 (reduced mod L1 / L2), (m1 + m2) & 1
   int occ_alias = 0;               // some occupied cells alias (M1 > L1 or M2 > L2)
   cudaStream_t aux = nullptr;      // second stream for the sub-batch split (created lazily)
+  double* beta_dev = nullptr;      // momentum table of the small-grid persistent solver
+  size_t beta_cap = 0;
+  std::vector<double> beta_host;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool full() const { return ax1.K == L1 && ax2.K == L2; }
 };
@@ -277,6 +280,7 @@ static void free_plan(bccb_plan_s* p) {
   cudaFree(p->lam_box_dev);
   cudaFree(p->occ_dev);
   if (p->aux) cudaStreamDestroy(p->aux);
+  cudaFree(p->beta_dev);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   cudaSetDevice(cur);
@@ -1144,6 +1148,86 @@ static int ensure_aux_stream(bccb_plan_s* p) {
   return BCCB_OK;
 }
 
+// ---- small-grid persistent solver (whole snapshot state in shared memory, all iterations in
+// one launch, one CTA per snapshot)
+static size_t small_smem(const bccb_plan_s* p, bool mom, int* trc_out) {
+  const AxisPrec& r = p->ax1.f;
+  const AxisPrec& c = p->ax2.s;
+  const size_t L = (size_t)p->L1 * p->L2;
+  const int nthr = std::max(p->L2 * r.R, 256);
+  const int trc = std::min(nthr / c.R, p->ax1.K);
+  if (trc_out) *trc_out = trc;
+  const int p1 = (r.R % 2 == 1) ? r.R : r.R + 1, p2 = (c.R % 2 == 1) ? c.R : c.R + 1;
+  const size_t rows_scr = (size_t)p->L2 * (p->ax1.K + 1) + (size_t)p->L2 * r.KP * p1;
+  const size_t cols_scr = (size_t)trc * (p->ax2.K + 1) + (size_t)trc * c.KP * p2;
+  return L * 16 + (mom ? L * 8 : 0) + 2 * (size_t)p->ax1.K * p->L2 * 8 + std::max(rows_scr, cols_scr) * 8;
+}
+
+static bool small_supported(const bccb_plan_s* p, const void* extra, bool mom) {
+  static const int env = [] {
+    const char* e = getenv("BCCB_SMALL_GRID");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env || extra) return false;
+  const AxisPrec& r = p->ax1.f;
+  const AxisPrec& c = p->ax2.s;
+  if ((long long)p->L2 * r.R > 1024) return false;
+  int trc = 0;
+  if (small_smem(p, mom, &trc) > 220 * 1024) return false;
+  if (trc < 1 || p->ax1.K % trc != 0) return false;
+  const int key = r.KP * 100 + c.KP;
+  return key == 1616 || key == 3216 || key == 1608 || key == 808 || key == 3208;
+}
+
+static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const EpiFista& e, const float2* D,
+                        const float2* P, const float2* Bh, cudaStream_t st) {
+  const bool mom = e.momentum != 0;
+  const int t_end = first + iters;
+  if (p->beta_cap < (size_t)t_end + 1) {
+    cudaFree(p->beta_dev);
+    p->beta_dev = nullptr;
+    p->beta_cap = std::max<size_t>((size_t)t_end + 1, 1024);
+    CUDA_TRY(cudaMalloc(&p->beta_dev, p->beta_cap * sizeof(double)));
+  }
+  p->beta_host.assign((size_t)t_end + 1, 0.0);
+  double alpha = 1.0;
+  for (int t = 1; t <= t_end; ++t) {
+    const double an = 0.5 * (std::sqrt(1.0 + 4.0 * alpha * alpha) + 1.0);
+    p->beta_host[t] = (alpha - 1.0) / an;
+    alpha = an;
+  }
+  CUDA_TRY(cudaMemcpyAsync(p->beta_dev, p->beta_host.data(), p->beta_host.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, st));
+  SmallArgs A;
+  A.ax1 = p->ax1.dev<float2>();
+  A.ax2 = p->ax2.dev_s();
+  A.cio = ColsIO<float2>{};
+  A.cio.D = D;
+  A.cio.P = P;
+  A.cio.Bh = Bh;
+  A.cio.K1 = p->ax1.K;
+  A.epi = e;
+  A.beta = p->beta_dev;
+  A.L1 = p->L1;
+  A.L2 = p->L2;
+  A.K1 = p->ax1.K;
+  A.K2 = p->ax2.K;
+  A.iterations = iters;
+  A.first_iteration = first;
+  LaunchShape sh;
+  sh.smem = small_smem(p, mom, &A.TRc);
+  sh.threads = std::max(p->L2 * p->ax1.f.R, 256);
+  sh.TR = 1;
+  const int key = p->ax1.f.KP * 100 + p->ax2.s.KP;
+#define SMALL_CASE(KP1_, KP2_)                                                                         \
+  if (key == KP1_ * 100 + KP2_)                                                                        \
+    return mom ? launch_pass<float2>(small_fista_kernel<KP1_, KP2_, true>, KIND_ROWS, (unsigned)batch, sh, st, A) \
+               : launch_pass<float2>(small_fista_kernel<KP1_, KP2_, false>, KIND_ROWS, (unsigned)batch, sh, st, A);
+  SMALL_CASE(16, 16) SMALL_CASE(32, 16) SMALL_CASE(16, 8) SMALL_CASE(8, 8) SMALL_CASE(32, 8)
+#undef SMALL_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no small-grid specialisation");
+}
+
 extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int iterations,
                               double mu, const double* tau,
                               const void* bhat_box, const void* extra, void* c, void* d,
@@ -1181,6 +1265,10 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
       alpha = an;
     }
   }
+  // small grids: the whole solve in one persistent launch per snapshot (shared-memory state)
+  if (small_supported(p, extra, e.momentum != 0))
+    return launch_small(p, batch, first_iteration, iterations, e, (const float2*)w.D, (const float2*)w.P,
+                        (const float2*)bhat_box, st);
   // specialised shapes use zero-segment skipping: flags start all-ones (read everything) and
   // the skipped zeros are written back by one final pass
   const bool zs = fast_supported(p, batch, extra);

@@ -230,7 +230,7 @@ struct ColsIO {
 // Column lines [row0, row0 + TR) (line = (snapshot b, column k1): length L2, band K2) processed
 // by one CTA of TR * ax.R threads (threads beyond that idle).  Shared by cols_kernel and the
 // fused rows kernel.  smem: TR x (K+1) band tile + TR x KP x pitch transpose buffer.
-template <int KP, typename C>
+template <int KP, typename C, bool U_GLOBAL = true>
 __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, const ColsIO<C>& io, long long row0,
                                            int TR, C* smem) {
   const int R = ax.R, K = ax.K, N = ax.N;
@@ -247,7 +247,7 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     if (active) {
       const C* line = io.U + gr * N + s;
 #pragma unroll
-      for (int r = 0; r < KP; ++r) a[r] = __ldcg(line + (long long)R * r);  // L2: written this launch
+      for (int r = 0; r < KP; ++r) a[r] = U_GLOBAL ? __ldcg(line + (long long)R * r) : line[(long long)R * r];
       reg_dft<KP, false>(a);
       band_fwd_scatter<KP>(a, s, ax, S + ii * SP);
     }
@@ -946,6 +946,137 @@ __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_z_kernel(Geo 
 #pragma unroll
   for (int r = 0; r < KP; ++r)
     if (!((fl >> r) & 1u)) zp[r * R] = make_float2(0.f, 0.f);
+}
+
+// ---------------------------------------------------------------- small-grid persistent solver
+// K5 of SURVEY.md: when a snapshot's whole state fits in shared memory (config 1: 64 x 64,
+// c 64 KB + d 32 KB), one CTA per snapshot runs ALL T iterations in one launch: rows pass
+// (band IFFT of V, fused epilogue, band FFT -> U), then the column pass (U -> V), both out of
+// shared memory, separated only by __syncthreads.  No HBM traffic and no launches per iteration.
+struct SmallArgs {
+  AxisT<float2> ax1;      // rows axis (complex64 engine)
+  AxisT<float2> ax2;      // columns axis (KP <= 16 engine)
+  ColsIO<float2> cio;     // D, P, Bh (global); U, V replaced by shared arrays in the kernel
+  EpiFista epi;           // c, d (global, per batch), tau, first_bad, a, kscale
+  const double* beta;     // [T + 1] momentum coefficients (FISTA)
+  int L1, L2, K1, K2;
+  int iterations, first_iteration;
+  int TRc;                // column lines per block pass
+};
+
+template <int KP1, int KP2, bool MOM>
+__global__ void __launch_bounds__(1024, 1) small_fista_kernel(SmallArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L1 = A.L1, L2 = A.L2, L = L1 * L2, K1 = A.K1;
+  const int b = blockIdx.x;
+  // shared layout: c [L] double2 | d [L] float2 | U [K1*L2] | V [K1*L2] | scratch
+  double2* cs = reinterpret_cast<double2*>(smem_raw);
+  float2* ds = reinterpret_cast<float2*>(cs + L);
+  float2* Us = ds + (MOM ? L : 0);
+  float2* Vs = Us + K1 * L2;
+  float2* scratch = Vs + K1 * L2;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  double2* cg = A.epi.c + (long long)b * L;
+  float2* dg = MOM ? A.epi.d + (long long)b * L : nullptr;
+  for (int i = tid; i < L; i += nthr) {
+    cs[i] = cg[i];
+    if (MOM) ds[i] = dg[i];
+  }
+  EpiFista e = A.epi;
+  e.c = cs;                      // shared-memory state; positions are local to the snapshot
+  e.d = MOM ? ds : nullptr;
+  e.extra = nullptr;
+  e.tau = A.epi.tau + b;         // the epilogue indexes tau[0] / first_bad[0] for this CTA
+  e.first_bad = A.epi.first_bad + b;
+  const AxisT<float2>& ax = A.ax1;
+  const int R = ax.R, K = ax.K, TR = L2;   // all rows of the snapshot at once
+  const double kap = e.kscale * e.tau[0];
+  const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
+  const int ii = tid / R, s = tid % R;
+  const bool active = tid < TR * R;
+  float2* Xs = scratch;
+  float2* S = scratch + TR * (K + 1);
+  const int SP = KP1 * ax.pitch;
+  // column pass geometry (one snapshot, lines = K1), shared-memory U / V
+  ColsIO<float2> cio = A.cio;
+  cio.U = Us;
+  cio.V = Vs;
+  cio.Bh = A.cio.Bh + (long long)b * K1 * A.K2;
+  Geo gc;
+  gc.L1 = L1;
+  gc.L2 = L2;
+  gc.rows = K1;
+  gc.TR = A.TRc;
+  gc.do_fwd = 1;
+  gc.do_inv = 1;
+  __syncthreads();
+  const int t_end = A.first_iteration + A.iterations;
+  for (int t = A.first_iteration - 1; t < t_end; ++t) {
+    const bool inv = t >= A.first_iteration;
+    const bool fwd = t + 1 < t_end;
+    float2 a[KP1];
+    // ---- rows pass: V (shared, [k1][l2]) -> per-line band tile -> g -> epilogue -> forward
+    if (inv) {
+      for (int idx = tid; idx < TR * K; idx += nthr) {
+        const int k = idx / TR, i2 = idx % TR;
+        Xs[i2 * (K + 1) + k] = Vs[k * L2 + i2];
+      }
+      __syncthreads();
+      if (active) band_inverse<KP1>(Xs + ii * (K + 1), s, ax, a);
+    }
+    if (active) {
+      e.it = t;
+      e.beta_cur = MOM ? A.beta[inv ? t : A.first_iteration] : 0.0;
+      e.beta_next = MOM ? A.beta[t + 1] : 0.0;
+#pragma unroll
+      for (int r = 0; r < KP1; ++r) {
+        const int pos = ii * L1 + s + R * r;
+        if (inv) {
+          const double2 cc = cs[pos];
+          const float2 dd = MOM ? ds[pos] : make_float2(0.f, 0.f);
+          const float2 g = a[r];
+          // zero fast path (bitwise identical, see rows_fista_fast_kernel)
+          if ((cc.x == 0.0) & (cc.y == 0.0) & (!MOM | ((dd.x == 0.f) & (dd.y == 0.f))) &&
+              fmaf(g.x, g.x, g.y * g.y) < kap2_lo) {
+            a[r] = make_float2(0.f, 0.f);
+            continue;
+          }
+          double2 cn;
+          float2 dn;
+          a[r] = e.step(cc, dd, g, make_float2(0.f, 0.f), 0, cn, dn);
+          cs[pos] = cn;
+          if (MOM) ds[pos] = dn;
+        } else {
+          a[r] = e.load(pos, 0);
+        }
+      }
+    }
+    if (!fwd) break;
+    __syncthreads();
+    if (active) {
+      reg_dft<KP1, false>(a);
+      band_fwd_scatter<KP1>(a, s, ax, S + ii * SP);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < TR * K; idx += nthr) {
+      const int i2 = idx / K, o = idx % K;
+      Xs[i2 * (K + 1) + o] = band_fwd_output(S + i2 * SP, o, KP1, ax);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < TR * K; idx += nthr) {
+      const int k = idx / TR, i2 = idx % TR;
+      Us[k * L2 + i2] = Xs[i2 * (K + 1) + k];
+    }
+    __syncthreads();
+    // ---- column pass: U -> V (all K1 lines of this snapshot)
+    for (int l0 = 0; l0 < K1; l0 += A.TRc) cols_block<KP2, float2, false>(gc, A.ax2, cio, l0, A.TRc, scratch);
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int i = tid; i < L; i += nthr) {
+    cg[i] = cs[i];
+    if (MOM) dg[i] = ds[i];
+  }
 }
 
 // Final pass of a zero-skipping run: write the zeros of every clear segment back so c (and d)
