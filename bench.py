@@ -207,7 +207,7 @@ def main():
     fb = torch.empty(B, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     if w.solver == "admm":
-        s1 = torch.zeros((B, L), dtype=torch.complex64, device=dev)     # z
+        s1 = torch.zeros((B, L), dtype=torch.complex128, device=dev)    # z
         s2 = torch.zeros((B, L), dtype=torch.complex128, device=dev)    # v (float64 dual)
         run = lambda: _lib.check(_lib.lib.bccb_admm_run(  # noqa: E731
             op._plan, B, 0, T, float(w.rho), tau_dev.data_ptr(), bhat.data_ptr(), None, s1.data_ptr(),
@@ -311,9 +311,11 @@ def main():
     e2e = None
     if not args.no_e2e:
         y_host = torch.from_numpy(y_np.astype(np.complex64)).pin_memory()
-        out_host = torch.empty((B, L), dtype=torch.complex64).pin_memory()
         k = min(w.targets, 64)
-        idx_host = torch.empty((B, k), dtype=torch.int32).pin_memory()
+        # rank 0 receives every rank's spectra and peak lists (one NCCL all-gather after the loop)
+        rows_out = B * world if rank == 0 else B
+        out_host = torch.empty((rows_out, L), dtype=torch.complex64).pin_memory()
+        idx_host = torch.empty((rows_out, k), dtype=torch.int32).pin_memory()
         cfg = bb.SolverConfig(iterations=T, step_size_mu=mu, rho=w.rho)
         solve = {"ista": bb.ista_solve, "fista": bb.fista_solve, "admm": bb.admm_solve}[w.solver]
 
@@ -323,8 +325,12 @@ def main():
             r = solve(p, cfg)
             est = r.estimate.to(torch.complex64)
             idx, _ = bb.topk_peaks(est, k)
-            out_host.copy_(est, non_blocking=True)
-            idx_host.copy_(idx, non_blocking=True)
+            if world > 1:
+                est = bdist.gather_rows(est, B * world)
+                idx = bdist.gather_rows(idx, B * world)
+            if est is not None:
+                out_host.copy_(est, non_blocking=True)
+                idx_host.copy_(idx, non_blocking=True)
             torch.cuda.synchronize(dev)
 
         for _ in range(max(1, args.warmup)):
@@ -340,10 +346,11 @@ def main():
             barrier()
         e_s = bdist.max_over_ranks(statistics.mean(et))
         e2e = {"value": world * gpi_step / e_s, "unit": UNIT, "ms_per_step": e_s * 1e3,
-               "h2d_bytes_per_step": int(y_host.numel() * 8),
-               "d2h_bytes_per_step": int(out_host.numel() * 8 + idx_host.numel() * 4),
-               "path": "LassoProblem.from_measurements (GPU A^H y) -> fista_solve -> topk_peaks; pinned host y in, "
-                       "complex64 spectra + peak indices out"}
+               "h2d_bytes_per_step": int(world * y_host.numel() * 8),
+               "d2h_bytes_per_step": int(world * B * L * 8 + world * B * k * 4),
+               "path": ("LassoProblem.from_measurements (GPU A^H y) -> solve -> topk_peaks"
+                        + (" -> NCCL all-gather of spectra + peaks to rank 0" if world > 1 else "")
+                        + "; pinned host y in (every rank), complex64 spectra + peak indices out (rank 0)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

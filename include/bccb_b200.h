@@ -133,7 +133,7 @@ int bccb_fista_run(bccb_plan_t plan, int batch, int first_iteration, int iterati
  * Replaces admm_solve (solvers.py:385-448): precompute P = (G + rho I)^-1, q = P b
  * (403-415) folded into the spectral box; loop c = q + rho P(z - v), z = S_{rho tau}(c + v),
  * v = v + (c - z) (426-436).
- *   z        : device complex64  [batch][L2][L1] (in: initial z; out: final z = the estimate)
+ *   z        : device complex128 [batch][L2][L1] (in: initial z; out: final z = the estimate)
  *   v        : device complex128 [batch][L2][L1] scaled dual (in: zeros; out: final)
  *   c_last   : device complex128 [batch][L2][L1] <- c of the last iteration (may be NULL)
  * Runs on the complex128 band engine: v grows like t*|q| when z stays 0 (config 3, SURVEY
@@ -172,6 +172,12 @@ int bccb_profile_end(double* ms_by_kind, long long* launches_by_kind);
 /* Number of streams a large batch is split over (1 or 2; default 2, env BCCB_SUBSTREAMS).
  * The halves are independent snapshots, so results are bitwise identical either way. */
 int bccb_set_substreams(int n);
+
+/* Kernel path: 0 = automatic (small-grid persistent solver, shape-specialised and fused
+ * kernels, generic fallback), 1 = generic runtime-shape kernels only.  Results agree to
+ * floating-point rounding (the paths evaluate the soft threshold with different float64
+ * sequences); used to cross-check the specialised kernels. */
+int bccb_set_path(int path);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,7 @@ SIGNATURES = {
     "bccb_profile_begin": (_i, []),
     "bccb_profile_end": (_i, [_vp, _vp]),
     "bccb_set_substreams": (_i, [_i]),
+    "bccb_set_path": (_i, [_i]),
 }
 
 

@@ -613,32 +613,24 @@ static int num_sms() {
   return g_num_sms;
 }
 
-constexpr int PIPE_STAGES = 8;
+// Kernel-path selection: 0 = automatic (small-grid persistent solver, specialised + fused
+// shapes, generic fallback); 1 = generic runtime-shape kernels only.  Env BCCB_ROWS_VARIANT
+// sets the default; bccb_set_path() overrides it (used by the tests to cross-check paths).
+static std::atomic<int> g_path{-1};
 
-template <int KP, bool MOM, bool EXTRA>
-static int launch_fista_pipe(const bccb_plan_s* p, const Geo& G, const AxisT<float2>& ax,
-                             const RowsIO<float2>& io, const EpiFista& epi, const LaunchShape& sh,
-                             cudaStream_t st) {
-  constexpr int CH = KP < 2 ? KP : 2;
-  constexpr int STG = PIPE_STAGES;
-  const long long tiles = (G.rows + G.TR - 1) / G.TR;
-  LaunchShape s2 = sh;
-  const size_t per = (size_t)STG * CH * sh.threads;
-  s2.smem += per * (sizeof(double2) + (MOM ? sizeof(float2) : 0) + (EXTRA ? sizeof(float2) : 0));
-  if (s2.smem > 227 * 1024) return -1;  // caller falls back to the register-pipelined kernel
-  const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)num_sms());
-  return launch_pass<float2>(rows_fista_pipe_kernel<KP, CH, STG, MOM, EXTRA>, KIND_ROWS, grid, s2, st, G, ax,
-                             io, epi, tiles);
+static int rows_variant() {
+  int v = g_path.load();
+  if (v < 0) {
+    const char* e = getenv("BCCB_ROWS_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
-// BCCB_ROWS_VARIANT: 0 = specialised shapes (default) else register-pipelined generic,
-// 1 = generic only, 2 = persistent cp.async ring.
-static int rows_variant() {
-  static int v = [] {
-    const char* e = getenv("BCCB_ROWS_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
+extern "C" int bccb_set_path(int path) {
+  if (path < 0 || path > 1) return fail(BCCB_ERR_INVALID, "path must be 0 (auto) or 1 (generic)");
+  g_path.store(path);
+  return BCCB_OK;
 }
 
 // Specialised line shapes (compile-time KP, R, Mo) of the FISTA/ISTA rows pass.
@@ -822,7 +814,7 @@ static int launch_rows_admm_fast(const bccb_plan_s* p, int batch, bool inv, bool
   return fail(BCCB_ERR_UNSUPPORTED, "no ADMM specialisation for this line shape");
 }
 
-static int launch_zero_segments_z(const bccb_plan_s* p, int batch, const Workspace& w, float2* z, cudaStream_t st) {
+static int launch_zero_segments_z(const bccb_plan_s* p, int batch, const Workspace& w, double2* z, cudaStream_t st) {
   LaunchShape sh = admm_shape(p);
   const Geo G = rows_geo(p, batch, sh, false, false);
   sh.smem = 0;
@@ -853,8 +845,7 @@ static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace
   return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
 }
 
-// Generic rows pass (runtime line shape): register-pipelined kernel, or the persistent cp.async
-// ring with BCCB_ROWS_VARIANT=2.
+// Generic rows pass (runtime line shape): register-pipelined kernel.
 static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                              const EpiFista& epi, cudaStream_t st) {
   const LaunchShape sh = shape_for<float2>(p->ax1);
@@ -862,17 +853,6 @@ static int launch_rows_fista(const bccb_plan_s* p, int batch, bool inv, bool fwd
   RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   const AxisT<float2> ax = p->ax1.dev<float2>();
-  const bool mom = epi.momentum != 0, extra = epi.extra != nullptr;
-  if (rows_variant() == 2 && inv) {
-    int rc = -1;
-    KP_DISPATCH_F(ax.KP, {
-      if (mom && !extra) rc = launch_fista_pipe<KPC, true, false>(p, G, ax, io, epi, sh, st);
-      else if (mom && extra) rc = launch_fista_pipe<KPC, true, true>(p, G, ax, io, epi, sh, st);
-      else if (!mom && !extra) rc = launch_fista_pipe<KPC, false, false>(p, G, ax, io, epi, sh, st);
-      else rc = launch_fista_pipe<KPC, false, true>(p, G, ax, io, epi, sh, st);
-    });
-    if (rc >= 0) return rc;
-  }
   KP_DISPATCH_F(ax.KP, {
     constexpr int CH = KPC < 2 ? KPC : 2;
     return launch_pass<float2>(rows_fista_kernel<KPC, CH, 2>, KIND_ROWS, grid, sh, st, G, ax, io, epi);
@@ -1168,7 +1148,7 @@ static bool small_supported(const bccb_plan_s* p, const void* extra, bool mom) {
     const char* e = getenv("BCCB_SMALL_GRID");
     return e ? atoi(e) : 1;
   }();
-  if (!env || extra) return false;
+  if (!env || extra || rows_variant() != 0) return false;
   const AxisPrec& r = p->ax1.f;
   const AxisPrec& c = p->ax2.s;
   if ((long long)p->L2 * r.R > 1024) return false;
@@ -1368,7 +1348,7 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
   if ((rc = launch_coef<double2>(p, 2, rho, a, w, st))) return rc;
   if (first_iteration == 0 && (rc = reset_first_bad(first_bad, batch, st))) return rc;
   EpiAdmm e;
-  e.z = (float2*)z;
+  e.z = (double2*)z;
   e.v = (double2*)v;
   e.c_out = nullptr;
   e.extra = (const float2*)extra;
@@ -1394,7 +1374,7 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
     e.c_out = (t + 1 == t_end) ? (double2*)c_last : nullptr;
     if ((rc = rows(true, t + 1 < t_end))) return rc;
   }
-  if (zs && (rc = launch_zero_segments_z(p, batch, w, (float2*)z, st))) return rc;
+  if (zs && (rc = launch_zero_segments_z(p, batch, w, (double2*)z, st))) return rc;
   return BCCB_OK;
 }
 

@@ -120,11 +120,12 @@ struct EpiFista {
   }
 };
 
-// ADMM (complex128 engine): state z (complex64), v (complex128).
+// ADMM (complex128 engine): state z and v both complex128 (z - v cancels when the threshold is
+// small and z ~ c + v, so z needs the dual's precision).
 // u = z - v is the operator input; c = a*u + g (+extra); z' = S_kappa(c + v);
 // v' = v + (c - z'); u' = z' - v'.   reference: pkg/src/bccblasso/solvers.py:385-448.
 struct EpiAdmm {
-  float2* z;
+  double2* z;
   double2* v;
   double2* c_out;                  // optional: c of this iteration (last iteration only)
   const float2* __restrict__ extra;
@@ -133,13 +134,13 @@ struct EpiAdmm {
   double a, kscale, extra_scale;
   int it;
   __device__ __forceinline__ double2 load(long long pos, int) const {
-    const float2 zz = z[pos];
+    const double2 zz = z[pos];
     const double2 vv = v[pos];
-    return make_double2((double)zz.x - vv.x, (double)zz.y - vv.y);
+    return make_double2(zz.x - vv.x, zz.y - vv.y);
   }
-  __device__ __forceinline__ double2 step(float2 zz, double2 vv, double2 g, float2 e, int b,
-                                          float2& zn, double2& vn, double2& cc) const {
-    const double ur = (double)zz.x - vv.x, ui = (double)zz.y - vv.y;
+  __device__ __forceinline__ double2 step(double2 zz, double2 vv, double2 g, float2 e, int b,
+                                          double2& zn, double2& vn, double2& cc) const {
+    const double ur = zz.x - vv.x, ui = zz.y - vv.y;
     double cr = __fma_rn(a, ur, g.x);
     double ci = __fma_rn(a, ui, g.y);
     if (extra) {
@@ -159,12 +160,12 @@ struct EpiAdmm {
       nzr = sr * f;
       nzi = si * f;
     }
-    zn = make_float2((float)nzr, (float)nzi);
-    // v' = v + (c - z') on the stored z, so the reference identity
-    // v_t = v_{t-1} + (c_t - z_t) (pkg/tests/test_solvers.py:283-295) holds bitwise in float64.
-    vn = make_double2(vv.x + (cr - (double)zn.x), vv.y + (ci - (double)zn.y));
+    zn = make_double2(nzr, nzi);
+    // v' = v + (c - z'): the reference identity v_t = v_{t-1} + (c_t - z_t)
+    // (pkg/tests/test_solvers.py:283-295) holds bitwise in float64.
+    vn = make_double2(vv.x + (cr - nzr), vv.y + (ci - nzi));
     cc = make_double2(cr, ci);
-    return make_double2((double)zn.x - vn.x, (double)zn.y - vn.y);
+    return make_double2(nzr - vn.x, nzi - vn.y);
   }
 };
 
@@ -409,117 +410,6 @@ __global__ void __launch_bounds__(256, MINB) rows_fista_kernel(Geo G, AxisT<floa
     if (G.do_inv) __syncthreads();
     rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
   }
-}
-
-// ---------------------------------------------------------------- pipelined pass A (FISTA/ISTA)
-// cp.async helpers (LDGSTS): per-thread asynchronous global->shared copies that hold no
-// registers while in flight.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// Persistent pass A: every CTA walks row tiles blockIdx.x, +gridDim.x, ...; every thread
-// streams ITS OWN state elements (c: 16 B, d: 8 B) through a STAGES-deep ring of
-// CH-element chunks in shared memory.  The ring runs ahead across tile boundaries, so
-// the loads of tile k+1 are in flight while tile k does its band FFTs: the SM keeps
-// STAGES*CH*24 B per thread (~100 KB per SM) of reads outstanding without registers.
-// Shared memory: [Xs: TR x (K+1)] [S: TR x KP x pitch] [ring c] [ring d] [ring e].
-template <int KP, int CH, int STAGES, bool MOMENTUM, bool EXTRA>
-__global__ void __launch_bounds__(256, 1) rows_fista_pipe_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io,
-                                                                 EpiFista epi, long long num_tiles) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int NC = KP / CH;  // chunks per tile
-  const int R = ax.R, K = ax.K, TR = G.TR;
-  const int nthr = blockDim.x;
-  const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
-  float2* Xs = reinterpret_cast<float2*>(smem_raw);
-  float2* S = Xs + TR * (K + 1);
-  double2* ring_c = reinterpret_cast<double2*>(S + TR * KP * ax.pitch);
-  float2* ring_d = reinterpret_cast<float2*>(ring_c + STAGES * CH * nthr);
-  float2* ring_e = ring_d + (MOMENTUM ? STAGES * CH * nthr : 0);
-  const long long step = gridDim.x;
-
-  // issue the copies of chunk `seq` of this thread's sequence into ring slot seq % STAGES
-  auto issue = [&](long long seq) {
-    const long long k = seq / NC;
-    const int ch = (int)(seq - k * NC);
-    const long long tile = blockIdx.x + k * step;
-    if (tile < num_tiles) {
-      const long long gr = tile * TR + ii;
-      if (ii < TR && gr < G.rows) {
-        const int slot = (int)(seq % STAGES);
-        const long long base = gr * G.L1 + s + (long long)R * (ch * CH);
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int si = (slot * CH + q) * nthr + threadIdx.x;
-          const long long pos = base + (long long)R * q;
-          cp_async16(ring_c + si, epi.c + pos);
-          if (MOMENTUM) cp_async8(ring_d + si, epi.d + pos);
-          if (EXTRA) cp_async8(ring_e + si, epi.extra + pos);
-        }
-      }
-    }
-    cp_async_commit();  // uniform group count, empty groups included
-  };
-
-  long long seq_next = 0;
-  if (G.do_inv)
-    for (int q = 0; q < STAGES - 1; ++q) issue(seq_next++);
-
-  long long seq = 0;
-  for (long long tile = blockIdx.x; tile < num_tiles; tile += step) {
-    const long long row0 = tile * TR;
-    const long long gr = row0 + ii;
-    const bool active = (ii < TR) && (gr < G.rows);
-    const long long base = gr * G.L1 + s;
-    const int b = (int)(gr / G.L2);
-    float2 a[KP];
-    if (G.do_inv) {
-      rows_load_band(G, ax, io, Xs, row0);
-      __syncthreads();
-      if (active) band_inverse<KP>(Xs + ii * (K + 1), s, ax, a);
-#pragma unroll
-      for (int ch = 0; ch < NC; ++ch, ++seq) {
-        issue(seq_next++);                 // keep STAGES-1 chunks ahead
-        cp_async_wait<STAGES - 1>();       // this thread's chunk `seq` has landed
-        if (active) {
-          const int slot = (int)(seq % STAGES);
-#pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int si = (slot * CH + q) * nthr + threadIdx.x;
-            const int r = ch * CH + q;
-            const long long pos = base + (long long)R * r;
-            const double2 cc = ring_c[si];
-            const float2 dd = MOMENTUM ? ring_d[si] : make_float2(0.f, 0.f);
-            const float2 ee = EXTRA ? ring_e[si] : make_float2(0.f, 0.f);
-            double2 cnew;
-            float2 dnew;
-            a[r] = epi.step(cc, dd, a[r], ee, b, cnew, dnew);
-            epi.c[pos] = cnew;
-            if (MOMENTUM) epi.d[pos] = dnew;
-          }
-        }
-      }
-    } else if (active) {
-#pragma unroll
-      for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
-    }
-    if (G.do_fwd) {
-      __syncthreads();  // Xs / S reuse across tiles
-      rows_forward_store<KP>(G, ax, io, a, active, ii, s, Xs, S, row0);
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- specialised pass A (FISTA/ISTA)
@@ -815,7 +705,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   const int b = row0 / L2;
   const int l20 = row0 - b * L2;
   const long long vbase = (long long)b * K * L2 + l20;
-  float2* zp = epi.z + (long long)gr * G.L1 + s;
+  double2* zp = epi.z + (long long)gr * G.L1 + s;
   double2* vp = epi.v + (long long)gr * G.L1 + s;
   double2* cop = epi.c_out ? epi.c_out + (long long)gr * G.L1 + s : nullptr;
   const double kap = epi.kscale * epi.tau[b];
@@ -830,7 +720,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
       const int k = idx / TR, i2 = idx % TR;
       Xs[i2 * XP + k] = io.V[vbase + (long long)k * L2 + i2];
     }
-    float2 z0 = make_float2(0.f, 0.f), z1 = z0;
+    double2 z0 = make_double2(0.0, 0.0), z1 = z0;
     double2 v0 = make_double2(0.0, 0.0), v1 = v0;
     if (active) {
       if (fl & 1u) z0 = zp[0];
@@ -856,33 +746,33 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
     unsigned nfl = 0;
 #pragma unroll
     for (int r = 0; r < KP; ++r) {
-      const float2 zz = z0;
+      const double2 zz = z0;
       const double2 vv = v0;
       z0 = z1;
       v0 = v1;
       if (r + 2 < KP && active) {
-        z1 = ((fl >> (r + 2)) & 1u) ? zp[(r + 2) * R] : make_float2(0.f, 0.f);
+        z1 = ((fl >> (r + 2)) & 1u) ? zp[(r + 2) * R] : make_double2(0.0, 0.0);
         v1 = vp[(r + 2) * R];
       }
       const double2 g = a[r];
-      const double cr = __fma_rn(a_id, (double)zz.x - vv.x, g.x);
-      const double ci = __fma_rn(a_id, (double)zz.y - vv.y, g.y);
+      const double cr = __fma_rn(a_id, zz.x - vv.x, g.x);
+      const double ci = __fma_rn(a_id, zz.y - vv.y, g.y);
       if (active && !isfinite(cr + ci)) atomicMin(epi.first_bad + b, epi.it);
       const double sr = cr + vv.x, si = ci + vv.y;
       const double m2 = sr * sr + si * si;
-      float2 zn = make_float2(0.f, 0.f);
+      double2 zn = make_double2(0.0, 0.0);
       if (!(m2 <= kap2)) {
         const double f = 1.0 - kap * rsqrt(m2);
-        zn = make_float2((float)(sr * f), (float)(si * f));
+        zn = make_double2(sr * f, si * f);
       }
-      // v' = v + (c - z') on the stored z (bitwise identity of test_solvers.py:283-295)
-      const double2 vn = make_double2(vv.x + (cr - (double)zn.x), vv.y + (ci - (double)zn.y));
+      // v' = v + (c - z') (bitwise identity of test_solvers.py:283-295)
+      const double2 vn = make_double2(vv.x + (cr - zn.x), vv.y + (ci - zn.y));
       if (active) {
         vp[r * R] = vn;
         if (cop) cop[r * R] = make_double2(cr, ci);
       }
       if (ZS) {
-        const bool nzv = (zn.x != 0.f) | (zn.y != 0.f);
+        const bool nzv = (zn.x != 0.0) | (zn.y != 0.0);
         if (__any_sync(0xffffffffu, nzv)) {
           if (active) zp[r * R] = zn;
           nfl |= 1u << r;
@@ -890,15 +780,15 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
       } else if (active) {
         zp[r * R] = zn;
       }
-      a[r] = make_double2((double)zn.x - vn.x, (double)zn.y - vn.y);
+      a[r] = make_double2(zn.x - vn.x, zn.y - vn.y);
     }
     if (ZS && lane == 0) *fw = nfl;
   } else if (active) {
 #pragma unroll
     for (int r = 0; r < KP; ++r) {
-      const float2 zz = ((fl >> r) & 1u) ? zp[r * R] : make_float2(0.f, 0.f);
+      const double2 zz = ((fl >> r) & 1u) ? zp[r * R] : make_double2(0.0, 0.0);
       const double2 vv = vp[r * R];
-      a[r] = make_double2((double)zz.x - vv.x, (double)zz.y - vv.y);
+      a[r] = make_double2(zz.x - vv.x, zz.y - vv.y);
     }
   }
   if (!G.do_fwd) return;
@@ -933,7 +823,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
 
 // Final zero pass for z of a zero-skipping ADMM run.
 template <int KP, int R>
-__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_z_kernel(Geo G, float2* z,
+__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_z_kernel(Geo G, double2* z,
                                                                             const unsigned* __restrict__ flags) {
   constexpr int NT = R > 256 ? R : 256;
   constexpr int TR = NT / R;
@@ -942,10 +832,10 @@ __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_z_kernel(Geo 
   const int gr = blockIdx.x * TR + ii;
   if (gr >= (int)G.rows) return;
   const unsigned fl = flags[(long long)blockIdx.x * (NT / 32) + (tid >> 5)];
-  float2* zp = z + (long long)gr * G.L1 + s;
+  double2* zp = z + (long long)gr * G.L1 + s;
 #pragma unroll
   for (int r = 0; r < KP; ++r)
-    if (!((fl >> r) & 1u)) zp[r * R] = make_float2(0.f, 0.f);
+    if (!((fl >> r) & 1u)) zp[r * R] = make_double2(0.0, 0.0);
 }
 
 // ---------------------------------------------------------------- small-grid persistent solver
@@ -1127,8 +1017,8 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, AxisT<double2> ax
 #pragma unroll
       for (int r = 0; r < KP; ++r) a[r] = epi.load(base + (long long)R * r, b);
     } else {
-      float2 zb[CH], eb[CH];
-      double2 vb[CH];
+      double2 zb[CH], vb[CH];
+      float2 eb[CH];
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
         const long long pos = base + (long long)R * q;
@@ -1138,8 +1028,8 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, AxisT<double2> ax
       }
 #pragma unroll
       for (int r0 = 0; r0 < KP; r0 += CH) {
-        float2 zn[CH], en[CH];
-        double2 vn[CH];
+        double2 zn[CH], vn[CH];
+        float2 en[CH];
         if (r0 + CH < KP) {
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
@@ -1152,8 +1042,7 @@ __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, AxisT<double2> ax
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
           const long long pos = base + (long long)R * (r0 + q);
-          float2 znew;
-          double2 vnew, cc;
+          double2 znew, vnew, cc;
           a[r0 + q] = epi.step(zb[q], vb[q], a[r0 + q], eb[q], b, znew, vnew, cc);
           epi.z[pos] = znew;
           epi.v[pos] = vnew;

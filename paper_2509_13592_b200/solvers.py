@@ -407,7 +407,7 @@ def admm_solve(problem: LassoProblem, config: SolverConfig, iterate_callback=Non
     op = problem.gram
     t0 = time.perf_counter()
     bhat, extra, tau_dev = problem.device_data()
-    z = _initial_state(problem, config, torch.complex64)
+    z = _initial_state(problem, config, torch.complex128)
     v = torch.zeros(z.shape, dtype=torch.complex128, device=z.device)
     first_bad = torch.empty(problem.batch, dtype=torch.int32, device=z.device)
     ws = op.workspace(problem.batch)
@@ -455,7 +455,7 @@ def admm_solve_with_c(problem: LassoProblem, config: SolverConfig):
     where the reference's z is identically zero (SURVEY finding 7)."""
     op = problem.gram
     bhat, extra, tau_dev = problem.device_data()
-    z = _initial_state(problem, config, torch.complex64)
+    z = _initial_state(problem, config, torch.complex128)
     v = torch.zeros(z.shape, dtype=torch.complex128, device=z.device)
     c_last = torch.empty_like(v)
     first_bad = torch.empty(problem.batch, dtype=torch.int32, device=z.device)

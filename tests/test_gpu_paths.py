@@ -1,0 +1,155 @@
+"""GPU cross-checks of the kernel paths and edge cases.
+
+The solver picks, per shape, the small-grid persistent solver, the shape-specialised
+(zero-skipping, fused-column) kernels or the generic runtime-shape kernels.  These tests
+run the same problems through the automatic path and the generic path
+(`bccb_set_path(1)`), and through the float64 oracle, on the shapes and batch sizes the
+fast paths special-case.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2509_13592_b200 as bb
+from oracle import bccb_oracle as orc
+from paper_2509_13592_b200 import _lib, scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def assert_close(est, ref, tol):
+    """rel-L2 <= tol, or both exactly zero (ADMM's z stays 0 when rho*tau is large, SURVEY finding 7)."""
+    est, ref = np.asarray(est), np.asarray(ref)
+    if not ref.any():
+        assert not est.any()
+    else:
+        assert orc.rel_l2(est, ref) < tol
+
+
+@pytest.fixture
+def generic_path():
+    def run(fn):
+        _lib.check(_lib.lib.bccb_set_path(1))
+        try:
+            return fn()
+        finally:
+            _lib.check(_lib.lib.bccb_set_path(0))
+    return run
+
+
+def scene_problem(cfg, nsnap, iters=None):
+    w = scenes.workload(cfg)
+    geom, ys, _ = scenes.make_scene(w, range(nsnap))
+    op = bb.gram_operator(geom, w.l1, w.l2)
+    m1, m2 = geom.occupied_coordinates()
+    bs = np.stack([orc.adjoint_fft(m1, m2, w.l1, w.l2, y) for y in ys])
+    taus = np.array([w.tau_fraction * np.abs(b).max() for b in bs])
+    return w, geom, op, bs, taus
+
+
+@pytest.mark.parametrize("cfg,nsnap,iters", [(1, 3, 200), (2, 6, 150), (4, 2, 60), (5, 1, 8)])
+def test_fista_auto_vs_generic_vs_oracle(cfg, nsnap, iters, generic_path):
+    w, geom, op, bs, taus = scene_problem(cfg, nsnap)
+    mu = 1.0 / (w.l1 * w.l2)
+    prob = bb.LassoProblem(op, bs, taus)
+    conf = bb.SolverConfig(iterations=iters, step_size_mu=mu)
+    auto = bb.fista_solve(prob, conf).estimate
+    gen = generic_path(lambda: bb.fista_solve(bb.LassoProblem(op, bs, taus), conf).estimate)
+    eig_t = np.ascontiguousarray(orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2).T)
+    for i in range(nsnap):
+        assert orc.rel_l2(auto[i], gen[i]) < 1e-6
+        ref = orc.fista(eig_t, bs[i], taus[i], mu, iters) if cfg != 5 or i == 0 else None
+        if ref is not None:
+            assert orc.rel_l2(auto[i], ref) < 1e-4
+            np.testing.assert_array_equal(np.sort(orc.topk(auto[i], w.targets)), np.sort(orc.topk(ref, w.targets)))
+
+
+@pytest.mark.parametrize("cfg,nsnap", [(1, 2), (2, 4)])
+def test_ista_auto_vs_generic(cfg, nsnap, generic_path):
+    w, geom, op, bs, taus = scene_problem(cfg, nsnap)
+    mu = 1.0 / (w.l1 * w.l2)
+    conf = bb.SolverConfig(iterations=120, step_size_mu=mu)
+    auto = bb.ista_solve(bb.LassoProblem(op, bs, taus), conf).estimate
+    gen = generic_path(lambda: bb.ista_solve(bb.LassoProblem(op, bs, taus), conf).estimate)
+    eig_t = np.ascontiguousarray(orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2).T)
+    for i in range(nsnap):
+        assert orc.rel_l2(auto[i], gen[i]) < 1e-6
+        assert orc.rel_l2(auto[i], orc.ista(eig_t, bs[i], taus[i], mu, 120)) < 1e-4
+
+
+def test_admm_auto_vs_generic_and_oracle(generic_path):
+    """Small threshold: z leaves zero, exercising the z-skipping kernel.  This regime is
+    ill-conditioned (points hover at the threshold: rounding b to complex64 moves the float64
+    answer by ~2e-3), so both sides get identical inputs: complex64 y, whose signed scatter
+    (the GPU's fft2(b) on the box) is exact."""
+    w = scenes.workload(3)
+    geom, ys, _ = scenes.make_scene(w, range(2))
+    op = bb.gram_operator(geom, w.l1, w.l2)
+    y32 = ys.astype(np.complex64)
+    m1, m2 = geom.occupied_coordinates()
+    bs = np.stack([orc.adjoint_fft(m1, m2, w.l1, w.l2, y.astype(np.complex128)) for y in y32])
+    taus = np.array([w.tau_fraction * np.abs(b).max() * 0.002 for b in bs])
+    conf = bb.SolverConfig(iterations=40, rho=1.0)
+    auto = bb.admm_solve(bb.LassoProblem.from_measurements(op, y32, tau=taus), conf).estimate
+    gen = generic_path(lambda: bb.admm_solve(bb.LassoProblem.from_measurements(op, y32, tau=taus), conf).estimate)
+    eig = orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2)
+    for i in range(2):
+        z, c, v = orc.admm(eig, bs[i], taus[i], 1.0, 40)
+        assert np.count_nonzero(z) > 0
+        assert orc.rel_l2(auto[i], gen[i]) < 1e-9
+        assert orc.rel_l2(auto[i], z) < 1e-6
+
+
+@pytest.mark.parametrize("m1,m2,l1,l2", [(6, 4, 9, 6), (5, 3, 12, 10), (4, 4, 20, 8), (3, 5, 7, 16)])
+def test_non_power_of_two_grids(m1, m2, l1, l2):
+    """Generic runtime-shape kernels: lengths with small power-of-two factors (KP = 1..4)."""
+    geom = bb.subsample_preserving_aperture(bb.make_ura(m1, m2), max(4, m1 * m2 // 2), seed=11)
+    op = bb.gram_operator(geom, l1, l2)
+    rng = np.random.default_rng(l1 * l2)
+    y = rng.standard_normal(geom.element_count) + 1j * rng.standard_normal(geom.element_count)
+    m1i, m2i = geom.occupied_coordinates()
+    b = orc.adjoint_fft(m1i, m2i, l1, l2, y)
+    np.testing.assert_allclose(bb.apply_adjoint(op, y), b, rtol=1e-5, atol=1e-5 * np.abs(b).max())
+    tau = 0.1 * np.abs(b).max()
+    mu = 1.0 / (l1 * l2)
+    eig = orc.gram_eigenvalues_exact(geom.occupancy, l1, l2)
+    eig_t = np.ascontiguousarray(eig.T)
+    r = bb.fista_solve(bb.LassoProblem(op, b, tau), bb.SolverConfig(iterations=50, step_size_mu=mu))
+    assert orc.rel_l2(r.estimate, orc.fista(eig_t, b, tau, mu, 50)) < 1e-5
+    r = bb.admm_solve(bb.LassoProblem(op, b, tau * 0.05), bb.SolverConfig(iterations=30, rho=2.0))
+    assert_close(r.estimate, orc.admm(eig, b, tau * 0.05, 2.0, 30)[0], 1e-4)
+
+
+def test_per_snapshot_divergence_in_a_batch():
+    w, geom, op, bs, taus = scene_problem(2, 4)
+    mu = 1.0 / (w.l1 * w.l2)
+    bad = bs.copy()
+    bad[2] *= 1e30                                    # overflows float64 after a few iterations
+    conf = bb.SolverConfig(iterations=60, step_size_mu=mu * 1e6)
+    with pytest.raises(bb.DivergenceError) as info:
+        bb.fista_solve(bb.LassoProblem(op, bad, taus), conf)
+    per = info.value.per_snapshot
+    assert per is not None and per[2] >= 0 and info.value.iteration == per[per >= 0].min()
+
+
+def test_admm_warm_start_and_torch_batch():
+    w, geom, op, bs, taus = scene_problem(2, 3)
+    eig = orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2)
+    z0 = np.zeros_like(bs)
+    z0[:, 5] = 0.01
+    bt = torch.as_tensor(bs).cuda()
+    r = bb.admm_solve(bb.LassoProblem(op, bt, torch.as_tensor(taus)), bb.SolverConfig(iterations=20, initial_c=z0))
+    assert isinstance(r.estimate, torch.Tensor) and r.estimate.shape == bt.shape
+    est = r.estimate.cpu().numpy()
+    for i in range(3):
+        assert_close(est[i], orc.admm(eig, bs[i], taus[i], 1.0, 20, z0=z0[i])[0], 1e-5)
+
+
+def test_extract_support_device_tensor():
+    c = torch.zeros(64, dtype=torch.complex128, device="cuda")
+    c[[3, 17, 40, 41]] = torch.tensor([2.0 - 1j, -5j, 0.2, 1.0 + 1.0j], dtype=torch.complex128, device="cuda")
+    g = bb.make_uniform_grid(8)
+    got = bb.extract_support(c, g, g, 0.1)
+    ref = orc.extract_support(c.cpu().numpy(), g.frequencies, g.frequencies, 0.1)
+    assert got == ref
