@@ -452,8 +452,25 @@ struct Workspace {
   int* counters;         // [batch] arrival counters of the fused column pass
 };
 
+// Rows engine of the specialised FISTA pass: the KP = 16 axis at 3 CTAs / SM for the shapes
+// that have it (half the register DFT => more resident warps to hide latency once the
+// iterate is sparse; measured +2-3% on configs 2 and 4), else the complex64 axis (KP <= 32).
+// BCCB_ROWS_KP16=0 selects the KP <= 32 engine everywhere.
+static int rows_kp16_env() {
+  static const int v = [] {
+    const char* e = getenv("BCCB_ROWS_KP16");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+static bool kp16_shape(const AxisPrec& a) {
+  return a.KP == 16 && ((a.R == 16 && a.Mo == 2) || (a.R == 64 && a.Mo == 4));
+}
+static bool rows_use_kp16(const AxisHost& ax) { return rows_kp16_env() && kp16_shape(ax.s); }
+static const AxisPrec& rows_axis(const AxisHost& ax) { return rows_use_kp16(ax) ? ax.s : ax.f; }
+
 // threads per CTA of the specialised FISTA rows pass (flags: one 32-bit word per warp)
-static int zs_threads(const AxisHost& ax) { return std::max(256, ax.f.R); }
+static int zs_threads(const AxisHost& ax) { return std::max(256, rows_axis(ax).R); }
 static size_t zs_flag_bytes(const bccb_plan_s* p, int batch);
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -467,7 +484,7 @@ static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R) {
 }
 
 // flags of the specialised FISTA rows pass (complex64 axis)
-static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, p->ax1.f.R); }
+static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, rows_axis(p->ax1).R); }
 
 // flags of the specialised ADMM rows pass (complex128 axis)
 static size_t zs_flag_bytes_d(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, p->ax1.d.R); }
@@ -650,7 +667,9 @@ static int fast_key(const AxisPrec& a) { return a.KP * 100000 + a.R * 10 + a.Mo;
 
 static bool fast_supported(const bccb_plan_s* p, int batch, const void* extra) {
   if (extra || rows_variant() != 0) return false;
-  const AxisPrec& a = p->ax1.f;
+  const AxisPrec& a = rows_axis(p->ax1);
+  if (rows_use_kp16(p->ax1))
+    return (long long)batch * p->L2 < (1LL << 31) && p->L2 % (zs_threads(p->ax1) / a.R) == 0;
   const int tr = zs_threads(p->ax1) / a.R;
   if ((long long)batch * p->L2 >= (1LL << 31) || p->L2 % tr != 0) return false;
   const int key = fast_key(a);
@@ -662,7 +681,7 @@ static bool fast_supported(const bccb_plan_s* p, int batch, const void* extra) {
 }
 
 static LaunchShape fast_shape(const bccb_plan_s* p) {
-  const AxisPrec& a = p->ax1.f;
+  const AxisPrec& a = rows_axis(p->ax1);
   LaunchShape sh;
   sh.threads = zs_threads(p->ax1);
   sh.TR = sh.threads / a.R;
@@ -673,9 +692,10 @@ static LaunchShape fast_shape(const bccb_plan_s* p) {
 
 // Fused column pass: enabled when one snapshot's column work (K1 x L2 points) is no more than
 // one rows CTA's work (TR x L1 points) and the shape has a fused specialisation.
-#define FUSED_SHAPES(X) \
-  X(16, 4, 1, 16)  /* config 1 */ \
-  X(32, 8, 1, 16)  /* config 2 */
+#define FUSED_SHAPES(X)                            \
+  X(16, 4, 1, 16, 2)  /* config 1 */              \
+  X(32, 8, 1, 16, 2)  /* config 2, KP 32 engine */ \
+  X(16, 16, 2, 16, 3) /* config 2, KP 16 engine */
 
 static bool fused_supported(const bccb_plan_s* p) {
   static const int env = [] {
@@ -683,14 +703,14 @@ static bool fused_supported(const bccb_plan_s* p) {
     return e ? atoi(e) : 1;
   }();
   if (!env) return false;
-  const AxisPrec& a = p->ax1.f;
+  const AxisPrec& a = rows_axis(p->ax1);
   const int tr = zs_threads(p->ax1) / a.R;
   if ((long long)p->ax1.K * p->L2 > (long long)tr * p->L1) return false;
   const AxisPrec& c = p->ax2.s;
   const int trc = std::min(zs_threads(p->ax1) / c.R, p->ax1.K);
   if (trc < 1 || p->ax1.K % trc != 0) return false;
   const int key = fast_key(a);
-#define FUSED_KEY(KP_, R_, MO_, KP2_) \
+#define FUSED_KEY(KP_, R_, MO_, KP2_, MINB_) \
   if (key == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_) return true;
   FUSED_SHAPES(FUSED_KEY)
 #undef FUSED_KEY
@@ -717,7 +737,7 @@ static FusedCols make_fused(const bccb_plan_s* p, int batch, const Workspace& w,
   fc.TRc = std::min(zs_threads(p->ax1) / c.R, p->ax1.K);
   fc.G.TR = fc.TRc;
   fc.counter = w.counters;
-  fc.cps = p->L2 / (zs_threads(p->ax1) / p->ax1.f.R);
+  fc.cps = p->L2 / (zs_threads(p->ax1) / rows_axis(p->ax1).R);
   fc.K1 = p->ax1.K;
   return fc;
 }
@@ -737,15 +757,30 @@ static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, boo
     const int pitch2 = (c.R % 2 == 1) ? c.R : c.R + 1;
     const size_t need = ((size_t)fused->TRc * (p->ax2.K + 1) + (size_t)fused->TRc * c.KP * pitch2) * sizeof(float2);
     sh.smem = std::max(sh.smem, need);
-#define FUSED_CASE(KP_, R_, MO_, KP2_)                                                                     \
-  if (key == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_)                                                 \
-    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true, KP2_>, KIND_ROWS, grid, sh,  \
-                                     st, G, ax, io, epi, fl, *fused)                                       \
-               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true, KP2_>, KIND_ROWS, grid, sh, \
-                                     st, G, ax, io, epi, fl, *fused);
+    const AxisT<float2> axr = rows_use_kp16(p->ax1) ? p->ax1.dev_s() : p->ax1.dev<float2>();
+    const int keyr = fast_key(rows_axis(p->ax1));
+#define FUSED_CASE(KP_, R_, MO_, KP2_, MINB_)                                                               \
+  if (keyr == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_)                                                 \
+    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true, KP2_, MINB_>, KIND_ROWS, grid, \
+                                     sh, st, G, axr, io, epi, fl, *fused)                                   \
+               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true, KP2_, MINB_>, KIND_ROWS, grid, \
+                                     sh, st, G, axr, io, epi, fl, *fused);
     FUSED_SHAPES(FUSED_CASE)
 #undef FUSED_CASE
     return fail(BCCB_ERR_UNSUPPORTED, "no fused specialisation for this line shape");
+  }
+  if (rows_use_kp16(p->ax1)) {
+    const AxisT<float2> axs = p->ax1.dev_s();
+    const FusedCols nofc16{};
+    const int k16 = fast_key(p->ax1.s);
+#define K16_CASE(R_, MO_)                                                                                \
+  if (k16 == 16 * 100000 + R_ * 10 + MO_)                                                                \
+    return mom ? launch_pass<float2>(rows_fista_fast_kernel<16, R_, MO_, true, true, 0, 3>, KIND_ROWS, grid, sh, \
+                                     st, G, axs, io, epi, fl, nofc16)                                    \
+               : launch_pass<float2>(rows_fista_fast_kernel<16, R_, MO_, false, true, 0, 3>, KIND_ROWS, grid, sh, \
+                                     st, G, axs, io, epi, fl, nofc16);
+    K16_CASE(16, 2) K16_CASE(64, 4)
+#undef K16_CASE
   }
   const FusedCols nofc{};
 #define FAST_CASE(KP_, R_, MO_)                                                                              \
@@ -835,8 +870,12 @@ static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace
   const Geo G = rows_geo(p, batch, sh, false, false);
   sh.smem = 0;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  const int key = fast_key(p->ax1.f);
   const unsigned* fl = (const unsigned*)w.flags;
+  if (rows_use_kp16(p->ax1)) {
+    if (p->ax1.s.R == 16) return launch_pass<float2>(zero_segments_kernel<16, 16>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (p->ax1.s.R == 64) return launch_pass<float2>(zero_segments_kernel<16, 64>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+  }
+  const int key = fast_key(p->ax1.f);
 #define ZERO_CASE(KP_, R_, MO_)                                                                           \
   if (key == KP_ * 100000 + R_ * 10 + MO_)                                                                \
     return launch_pass<float2>(zero_segments_kernel<KP_, R_>, KIND_OTHER, grid, sh, st, G, c, d, fl);

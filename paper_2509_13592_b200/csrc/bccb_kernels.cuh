@@ -473,8 +473,8 @@ struct FusedCols {
   int K1;
 };
 
-template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0>
-__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
+template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0, int MINB = 2>
+__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
     rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
                            FusedCols fc) {
   constexpr int NT = R > 256 ? R : 256;   // threads per CTA
