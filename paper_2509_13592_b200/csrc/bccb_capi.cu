@@ -686,7 +686,10 @@ static LaunchShape fast_shape(const bccb_plan_s* p) {
   sh.threads = zs_threads(p->ax1);
   sh.TR = sh.threads / a.R;
   const int pitch = (a.R % 2 == 1) ? a.R : a.R + 1;
-  sh.smem = ((size_t)sh.TR * (p->ax1.K + 1) + (size_t)sh.TR * a.KP * pitch) * sizeof(float2);
+  // band tile + transpose buffer (+ staged twiddles [KP][R], [Mo][R] when <= 8 KB: STAGE_TW)
+  const size_t tw = (size_t)(a.KP + a.Mo) * a.R;
+  sh.smem = ((size_t)sh.TR * (p->ax1.K + 1) + (size_t)sh.TR * a.KP * pitch + (tw * 8 <= 8192 ? tw : 0)) *
+            sizeof(float2);
   return sh;
 }
 

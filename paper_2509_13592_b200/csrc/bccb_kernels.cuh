@@ -488,7 +488,21 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* Xs = reinterpret_cast<float2*>(smem_raw);
   float2* S = Xs + TR * XP;
+  // Twiddles: staged in shared memory when the tables are small (<= 8 KB: short-latency LDS
+  // instead of L1 round trips, measured +1% at config 2); read through L1 otherwise (a 36 KB
+  // table at L1 = 4096 would cost a resident CTA per SM, measured -18% at config 5).
+  constexpr bool STAGE_TW = (KP + MO) * R * 8 <= 8192;
+  const float2* tw1s = ax.tw1;
+  const float2* tw2s = ax.tw2;
   const int tid = threadIdx.x;
+  if constexpr (STAGE_TW) {
+    float2* t1 = S + TR * SP;     // [KP][R] then [MO][R]
+    float2* t2 = t1 + KP * R;
+    for (int i2 = tid; i2 < KP * R; i2 += NT) t1[i2] = ax.tw1[i2];
+    for (int i2 = tid; i2 < MO * R; i2 += NT) t2[i2] = ax.tw2[i2];
+    tw1s = t1;
+    tw2s = t2;
+  }
   const int ii = tid / R, s = tid % R;
   const int row0 = blockIdx.x * TR;            // rows < 2^31 (host check)
   const int gr = row0 + ii;
@@ -533,12 +547,12 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
       for (int j = 0; j < KP; ++j) a[j] = Y[j];
 #pragma unroll
       for (int m = 1; m < MO; ++m) {
-        const float2 w2 = __ldg(ax.tw2 + m * R + s);
+        const float2 w2 = tw2s[m * R + s];
 #pragma unroll
         for (int j = 0; j < KP; ++j) a[j] = cadd(a[j], cmulc(Y[j + KP * m], w2));
       }
 #pragma unroll
-      for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], __ldg(ax.tw1 + j * R + s));
+      for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
       reg_dft<KP, true>(a);
       // ---- fused epilogue, register-pipelined state stream
 #pragma unroll
@@ -638,7 +652,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
     reg_dft<KP, false>(a);
     float2* Srow = S + ii * SP;
 #pragma unroll
-    for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], __ldg(ax.tw1 + j * R + s));
+    for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], tw1s[j * R + s]);
   }
   __syncthreads();
   for (int idx = tid; idx < TR * K; idx += NT) {
@@ -654,9 +668,9 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
 #pragma unroll
       for (int t = 0; t < R; ++t) acc = cadd(acc, row[t]);
     } else {
-      const float2* tw = ax.tw2 + m * R;
+      const float2* tw = tw2s + m * R;
 #pragma unroll
-      for (int t = 0; t < R; ++t) acc = cfma(row[t], __ldg(tw + t), acc);
+      for (int t = 0; t < R; ++t) acc = cfma(row[t], tw[t], acc);
     }
     Xs[i2 * XP + o] = acc;
   }
