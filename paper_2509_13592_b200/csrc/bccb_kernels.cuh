@@ -693,6 +693,17 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   }
 }
 
+// cp.async (LDGSTS): per-thread asynchronous global -> shared copies that hold no registers
+// while in flight.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 // ---------------------------------------------------------------- specialised pass A (ADMM)
 // Complex128 engine, compile-time line shape (KP <= 16, R, MO).  State: z (complex64, sparse:
 // zero-segment flags as in the FISTA kernel) and the scaled dual v (complex128, dense, always
@@ -729,18 +740,24 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   const unsigned fl = ZS ? *fw : 0xffffffffu;
   double2 a[KP];
 
+  // The dense dual v streams through shared memory: all KP values of a thread are requested
+  // with cp.async before the band inverse runs (no registers held; the fp64 inverse DFT hides
+  // the latency).  The staging aliases the transpose buffer S, which is free until the forward.
+  double2* vstage = S;   // [KP][NT]
   if (G.do_inv) {
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < KP; ++r) cp_async16(vstage + r * NT + tid, vp + r * R);
+    }
+    cp_async_commit();
     for (int idx = tid; idx < TR * K; idx += NT) {
       const int k = idx / TR, i2 = idx % TR;
       Xs[i2 * XP + k] = io.V[vbase + (long long)k * L2 + i2];
     }
     double2 z0 = make_double2(0.0, 0.0), z1 = z0;
-    double2 v0 = make_double2(0.0, 0.0), v1 = v0;
     if (active) {
       if (fl & 1u) z0 = zp[0];
       if ((fl >> 1) & 1u) z1 = zp[R];
-      v0 = vp[0];
-      v1 = vp[R];
     }
     __syncthreads();
     {
@@ -757,17 +774,14 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
       for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], __ldg(ax.tw1 + j * R + s));
       reg_dft<KP, true>(a);
     }
+    cp_async_wait_all();   // this thread's v values have landed
     unsigned nfl = 0;
 #pragma unroll
     for (int r = 0; r < KP; ++r) {
       const double2 zz = z0;
-      const double2 vv = v0;
+      const double2 vv = active ? vstage[r * NT + tid] : make_double2(0.0, 0.0);
       z0 = z1;
-      v0 = v1;
-      if (r + 2 < KP && active) {
-        z1 = ((fl >> (r + 2)) & 1u) ? zp[(r + 2) * R] : make_double2(0.0, 0.0);
-        v1 = vp[(r + 2) * R];
-      }
+      if (r + 2 < KP && active) z1 = ((fl >> (r + 2)) & 1u) ? zp[(r + 2) * R] : make_double2(0.0, 0.0);
       const double2 g = a[r];
       const double cr = __fma_rn(a_id, zz.x - vv.x, g.x);
       const double ci = __fma_rn(a_id, zz.y - vv.y, g.y);
@@ -806,6 +820,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
     }
   }
   if (!G.do_fwd) return;
+  __syncthreads();   // every thread is done with its v staging (aliases S)
   if (active) {
     reg_dft<KP, false>(a);
     double2* Srow = S + ii * SP;
