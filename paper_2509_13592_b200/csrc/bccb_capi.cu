@@ -1201,10 +1201,8 @@ static bool small_supported(const bccb_plan_s* p, const void* extra, bool mom) {
   return key == 1616 || key == 3216 || key == 1608 || key == 808 || key == 3208;
 }
 
-static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const EpiFista& e, const float2* D,
-                        const float2* P, const float2* Bh, cudaStream_t st) {
-  const bool mom = e.momentum != 0;
-  const int t_end = first + iters;
+// momentum coefficients beta_t, t <= t_end, in a plan-owned device table (persistent solvers)
+static int upload_beta(bccb_plan_s* p, int t_end, cudaStream_t st) {
   if (p->beta_cap < (size_t)t_end + 1) {
     cudaFree(p->beta_dev);
     p->beta_dev = nullptr;
@@ -1220,6 +1218,48 @@ static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const E
   }
   CUDA_TRY(cudaMemcpyAsync(p->beta_dev, p->beta_host.data(), p->beta_host.size() * sizeof(double),
                            cudaMemcpyHostToDevice, st));
+  return BCCB_OK;
+}
+
+// ---- 64 x 64 cluster solver (8-CTA cluster per snapshot, distributed shared memory)
+static bool cluster_supported(const bccb_plan_s* p, const void* extra) {
+  static const int env = [] {
+    const char* e = getenv("BCCB_CLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env || extra || rows_variant() != 0) return false;
+  const int K1 = p->ax1.K, K2 = p->ax2.K;
+  return p->L1 == 64 && p->L2 == 64 && K1 % 8 == 0 && K2 % 8 == 0 && K1 <= 16 && K2 <= 16;
+}
+
+static int launch_cluster64(bccb_plan_s* p, int batch, int first, int iters, const EpiFista& e, const float2* D,
+                            const float2* P, const float2* Bh, cudaStream_t st) {
+  int rc = upload_beta(p, first + iters, st);
+  if (rc) return rc;
+  ClusterArgs A;
+  A.D = D;
+  A.P = P;
+  A.Bh = Bh;
+  A.epi = e;
+  A.beta = p->beta_dev;
+  A.K1 = p->ax1.K;
+  A.K2 = p->ax2.K;
+  A.iterations = iters;
+  A.first_iteration = first;
+  LaunchShape sh;
+  sh.threads = 256;
+  sh.TR = 1;
+  sh.smem = 0;
+  const unsigned grid = (unsigned)batch * 8u;
+  return e.momentum ? launch_pass<float2>(cluster64_fista_kernel<true>, KIND_ROWS, grid, sh, st, A)
+                    : launch_pass<float2>(cluster64_fista_kernel<false>, KIND_ROWS, grid, sh, st, A);
+}
+
+static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const EpiFista& e, const float2* D,
+                        const float2* P, const float2* Bh, cudaStream_t st) {
+  const bool mom = e.momentum != 0;
+  int rc0 = upload_beta(p, first + iters, st);
+  if (rc0) return rc0;
   SmallArgs A;
   A.ax1 = p->ax1.dev<float2>();
   A.ax2 = p->ax2.dev_s();
@@ -1287,6 +1327,10 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
       alpha = an;
     }
   }
+  // 64 x 64 grids: one 8-CTA cluster per snapshot runs the whole solve (distributed shared memory)
+  if (cluster_supported(p, extra))
+    return launch_cluster64(p, batch, first_iteration, iterations, e, (const float2*)w.D, (const float2*)w.P,
+                            (const float2*)bhat_box, st);
   // small grids: the whole solve in one persistent launch per snapshot (shared-memory state)
   if (small_supported(p, extra, e.momentum != 0))
     return launch_small(p, batch, first_iteration, iterations, e, (const float2*)w.D, (const float2*)w.P,

@@ -12,6 +12,8 @@
 // Bhat / D / P boxes are [.][K1][K2].  The full-grid state never leaves its
 // [B][L2][L1] layout.  See DESIGN.md for the byte model.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "band_fft.cuh"
 
 namespace bccb {
@@ -995,6 +997,159 @@ __global__ void __launch_bounds__(1024, 1) small_fista_kernel(SmallArgs A) {
   for (int i = tid; i < L; i += nthr) {
     cg[i] = cs[i];
     if (MOM) dg[i] = ds[i];
+  }
+}
+
+// ---------------------------------------------------------------- 64 x 64 cluster solver
+// Config-1 shape (L1 = L2 = 64, band K1, K2 <= 16, multiples of 8): one thread-block CLUSTER of
+// 8 CTAs per snapshot runs all T iterations in one launch.  CTA r owns rows [8r, 8r+8) and the
+// column lines k1 in [r*K1/8, (r+1)*K1/8).  Band tiles move between CTAs through distributed
+// shared memory (map_shared_rank), two cluster barriers per iteration; the state never leaves
+// shared memory.  With lines of 64 points and bands of 16, direct band DFTs on the constant
+// 64th-root table are shorter dependency chains than FFT stages.
+struct ClusterArgs {
+  const float2* D;       // [K1][K2]
+  const float2* P;       // [K1][K2]
+  const float2* Bh;      // [B][K1][K2]
+  EpiFista epi;
+  const double* beta;    // [T + 1]
+  int K1, K2, iterations, first_iteration;
+};
+
+
+template <bool MOM>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 1) cluster64_fista_kernel(ClusterArgs A) {
+  namespace cgp = cooperative_groups;
+  constexpr int L = 64, CL = 8, RPC = L / CL;
+  cgp::cluster_group cluster = cgp::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / CL;
+  const int K1 = A.K1, K2 = A.K2, LPC = K1 / CL;   // column lines per CTA
+  const int tid = threadIdx.x;
+  __shared__ double2 cs[RPC * L];
+  __shared__ float2 ds[RPC * L];
+  __shared__ float2 xs[RPC * L];       // next operator input (forward DFT input)
+  __shared__ float2 Ul[16 * RPC];      // my rows' band: [k1][row]
+  __shared__ float2 Vl[16 * RPC];      // band input of my rows: [k1][row]
+  __shared__ float2 Vline[2 * L];      // my column lines after the column pass: [j][l2]
+  __shared__ float2 line[2 * L];       // my column lines gathered from U: [j][l2]
+  __shared__ float2 Yb[2 * 16];        // band values of my lines: [j][k2]
+  __shared__ float2 roots[64];         // e^{-2 pi i t / 64}: lane-varying indices -> shared, not constant
+  if (tid < 64) roots[tid] = c_roots64[tid];
+  auto w64 = [&](int t) { return roots[t & 63]; };
+  const long long base = ((long long)b * L + rank * RPC) * L;
+  for (int i = tid; i < RPC * L; i += 256) {
+    cs[i] = A.epi.c[base + i];
+    ds[i] = MOM ? A.epi.d[base + i] : make_float2(0.f, 0.f);
+  }
+  EpiFista e = A.epi;
+  e.c = cs;
+  e.d = MOM ? ds : nullptr;
+  e.extra = nullptr;
+  e.tau = A.epi.tau + b;
+  e.first_bad = A.epi.first_bad + b;
+  const double kap = e.kscale * e.tau[0];
+  const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
+  const float2* Bh = A.Bh + (long long)b * K1 * K2;
+  // loop-invariant spectral data of my column lines, hoisted out of global memory
+  __shared__ float2 Dl[2 * 16], PB[2 * 16];
+  for (int q = tid; q < LPC * K2; q += 256) {
+    const int j = q / K2, k2 = q % K2, k1 = rank * LPC + j;
+    Dl[j * 16 + k2] = A.D[k1 * K2 + k2];
+    PB[j * 16 + k2] = cmul(Bh[k1 * K2 + k2], A.P[k1 * K2 + k2]);
+  }
+  FistaScalars sc{kap, e.a, 0.0, 0, 0, e.first_bad};
+  __syncthreads();
+  const int t_end = A.first_iteration + A.iterations;
+  for (int t = A.first_iteration - 1; t < t_end; ++t) {
+    const bool inv = t >= A.first_iteration;
+    const bool fwd = t + 1 < t_end;
+    e.it = t;
+    e.beta_cur = MOM ? A.beta[inv ? t : A.first_iteration] : 0.0;
+    e.beta_next = MOM ? A.beta[t + 1] : 0.0;
+    sc.bc = e.beta_cur;
+    sc.it = t;
+    const float bn = (float)e.beta_next;
+    // ---- rows: inverse band DFT (direct), fused epilogue -> xs
+    for (int p = tid; p < RPC * L; p += 256) {
+      const int i = p / L, l1 = p % L;
+      float2 x;
+      if (inv) {
+        float2 g = make_float2(0.f, 0.f);
+        for (int k = 0; k < K1; ++k) g = cfma(Vl[k * RPC + i], cmake(w64(l1 * k).x, -w64(l1 * k).y), g);
+        const double2 cc = cs[p];
+        const float2 dd = MOM ? ds[p] : make_float2(0.f, 0.f);
+        if ((cc.x == 0.0) & (cc.y == 0.0) & (!MOM | ((dd.x == 0.f) & (dd.y == 0.f))) &&
+            fmaf(g.x, g.x, g.y * g.y) < kap2_lo) {
+          x = make_float2(0.f, 0.f);
+        } else {
+          float2 dn = make_float2(0.f, 0.f);
+          const double2 cn = fista_point_slow<MOM>(cc, dd, g, sc, &dn);
+          cs[p] = cn;
+          if (MOM) ds[p] = dn;
+          x = MOM ? make_float2(fmaf(bn, dn.x, (float)cn.x), fmaf(bn, dn.y, (float)cn.y))
+                  : make_float2((float)cn.x, (float)cn.y);
+        }
+      } else {
+        x = e.load(p, 0);
+      }
+      xs[p] = x;
+    }
+    if (!fwd) break;
+    __syncthreads();
+    // ---- rows: forward band DFT, U[k1][row] (2 lanes per output, 32 terms each)
+    for (int q = tid; q < 2 * K1 * RPC; q += 256) {
+      const int o = q >> 1, h = q & 1;
+      const int k = o / RPC, i = o % RPC;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int l1 = h * 32; l1 < h * 32 + 32; ++l1) acc = cfma(xs[i * L + l1], w64(l1 * k), acc);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      if (h == 0) Ul[k * RPC + i] = acc;
+    }
+    cluster.sync();   // every CTA's U tile is published
+    // ---- columns: gather my lines from the 8 row owners (DSMEM)
+    for (int q = tid; q < LPC * L; q += 256) {
+      const int j = q / L, l2 = q % L;
+      const int k1 = rank * LPC + j;
+      const float2* src = cluster.map_shared_rank(Ul, l2 / RPC);
+      line[j * L + l2] = src[k1 * RPC + (l2 % RPC)];
+    }
+    __syncthreads();
+    // forward column DFT to the band (8 lanes per output), spectral multiply-add
+    for (int q = tid; q < LPC * K2 * 8; q += 256) {
+      const int o = q >> 3, h = q & 7;
+      const int j = o / K2, k2 = o % K2;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int l2 = h * 8; l2 < h * 8 + 8; ++l2) acc = cfma(line[j * L + l2], w64(l2 * k2), acc);
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (h == 0) Yb[j * 16 + k2] = cadd(cmul(acc, Dl[j * 16 + k2]), PB[j * 16 + k2]);
+    }
+    __syncthreads();
+    // inverse column DFT of the band -> Vline[j][l2]
+    for (int q = tid; q < LPC * L; q += 256) {
+      const int j = q / L, l2 = q % L;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int k2 = 0; k2 < K2; ++k2) acc = cfma(Yb[j * 16 + k2], cmake(w64(l2 * k2).x, -w64(l2 * k2).y), acc);
+      Vline[q] = acc;
+    }
+    cluster.sync();   // every CTA's column lines are published
+    // ---- gather the band input of my rows from the line owners (DSMEM)
+    for (int q = tid; q < K1 * RPC; q += 256) {
+      const int k1 = q / RPC, i = q % RPC;
+      const float2* src = cluster.map_shared_rank(Vline, k1 / LPC);
+      Vl[q] = src[(k1 % LPC) * L + rank * RPC + i];
+    }
+    __syncthreads();
+  }
+  cluster.sync();   // no CTA may exit while others still read its shared memory
+  for (int i = tid; i < RPC * L; i += 256) {
+    A.epi.c[base + i] = cs[i];
+    if (MOM) A.epi.d[base + i] = ds[i];
   }
 }
 
