@@ -16,7 +16,7 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbccb_b200.so")
+LIB_PATH = os.environ.get("BCCB_LIB_PATH") or os.path.join(_HERE, "libbccb_b200.so")   # override: A/B of builds
 
 OK, ERR_INVALID, ERR_DIVERGENCE, ERR_SINGULAR, ERR_CUDA, ERR_UNSUPPORTED = range(6)
 

@@ -475,38 +475,65 @@ struct FusedCols {
   int K1;
 };
 
-template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0, int MINB = 2>
-__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
-    rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
-                           FusedCols fc) {
-  constexpr int NT = R > 256 ? R : 256;   // threads per CTA
-  constexpr int TR = NT / R;
-  constexpr int K = KP * MO;
-  constexpr int XP = K + 1;
-  constexpr int PITCH = (R % 2 == 1) ? R : R + 1;
-  constexpr int SP = KP * PITCH;
-  constexpr int CH = 2;
-  static_assert(KP % CH == 0, "chunking");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* Xs = reinterpret_cast<float2*>(smem_raw);
-  float2* S = Xs + TR * XP;
-  // Twiddles: staged in shared memory when the tables are small (<= 8 KB: short-latency LDS
-  // instead of L1 round trips, measured +1% at config 2); read through L1 otherwise (a 36 KB
-  // table at L1 = 4096 would cost a resident CTA per SM, measured -18% at config 5).
-  constexpr bool STAGE_TW = (KP + MO) * R * 8 <= 8192;
-  const float2* tw1s = ax.tw1;
-  const float2* tw2s = ax.tw2;
-  const int tid = threadIdx.x;
-  if constexpr (STAGE_TW) {
-    float2* t1 = S + TR * SP;     // [KP][R] then [MO][R]
+// acquire / release on a per-snapshot progress word (persistent solver)
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Shared-memory twiddle staging of the specialised rows pass: tables of at most 8 KB are
+// staged (short-latency LDS instead of L1 round trips, measured +1% at config 2); larger ones
+// are read through L1 (a 36 KB table at L1 = 4096 would cost a resident CTA per SM, measured
+// -18% at config 5).
+template <int KP, int R, int MO>
+struct TileShape {
+  static constexpr int NT = R > 256 ? R : 256;   // threads per CTA
+  static constexpr int TR = NT / R;              // lines per CTA
+  static constexpr int K = KP * MO;
+  static constexpr int XP = K + 1;
+  static constexpr int PITCH = (R % 2 == 1) ? R : R + 1;
+  static constexpr int SP = KP * PITCH;
+  static constexpr bool STAGE_TW = (KP + MO) * R * 8 <= 8192;
+};
+
+template <int KP, int R, int MO>
+__device__ __forceinline__ void stage_twiddles(const AxisT<float2>& ax, float2* dst, const float2*& tw1s,
+                                               const float2*& tw2s) {
+  using TS = TileShape<KP, R, MO>;
+  tw1s = ax.tw1;
+  tw2s = ax.tw2;
+  if constexpr (TS::STAGE_TW) {
+    float2* t1 = dst;     // [KP][R] then [MO][R]
     float2* t2 = t1 + KP * R;
-    for (int i2 = tid; i2 < KP * R; i2 += NT) t1[i2] = ax.tw1[i2];
-    for (int i2 = tid; i2 < MO * R; i2 += NT) t2[i2] = ax.tw2[i2];
+    for (int i2 = threadIdx.x; i2 < KP * R; i2 += TS::NT) t1[i2] = ax.tw1[i2];
+    for (int i2 = threadIdx.x; i2 < MO * R; i2 += TS::NT) t2[i2] = ax.tw2[i2];
     tw1s = t1;
     tw2s = t2;
   }
+}
+
+// One tile (TR lines of one snapshot) of the specialised FISTA rows pass.  `tile` indexes the
+// tile (and its flag words); with KP2 > 0 and do_fwd, the last tile of a snapshot to arrive
+// runs that snapshot's column pass and, in the persistent solver (done != null), publishes
+// `done[b] = step + 1`.  Streaming state / band loads bypass L1 (ld.global.cg): in the
+// persistent solver another SM wrote them in an earlier step.
+template <int KP, int R, int MO, bool MOM, bool ZS, int KP2>
+__device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
+                                                const EpiFista& epi, unsigned* __restrict__ flags,
+                                                const FusedCols& fc, int tile, const float2* tw1s,
+                                                const float2* tw2s, float2* Xs, int* done, int step) {
+  using TS = TileShape<KP, R, MO>;
+  constexpr int NT = TS::NT, TR = TS::TR, K = TS::K, XP = TS::XP, PITCH = TS::PITCH, SP = TS::SP;
+  constexpr int CH = 2;
+  static_assert(KP % CH == 0, "chunking");
+  float2* S = Xs + TR * XP;
+  const int tid = threadIdx.x;
   const int ii = tid / R, s = tid % R;
-  const int row0 = blockIdx.x * TR;            // rows < 2^31 (host check)
+  const int row0 = tile * TR;            // rows < 2^31 (host check)
   const int gr = row0 + ii;
   const bool active = gr < (int)G.rows;
   const int L2 = G.L2;
@@ -521,15 +548,20 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float bn = (float)epi.beta_next;
   const FistaScalars sc{kap, a_id, bc, b, epi.it, epi.first_bad};
   const int lane = tid & 31;
-  unsigned* fw = ZS ? flags + ((long long)blockIdx.x * (NT / 32) + (tid >> 5)) : nullptr;
-  const unsigned fl = ZS ? *fw : 0xffffffffu;
+  // flag words per tile: NT/32 warp words (zero segments), then one tile word (bit 0: the
+  // tile's U band may be nonzero; clear = U already holds zeros, the store can be skipped)
+  unsigned* fw = ZS ? flags + ((long long)tile * (NT / 32 + 1) + (tid >> 5)) : nullptr;
+  unsigned* tword = ZS ? flags + ((long long)tile * (NT / 32 + 1) + NT / 32) : nullptr;
+  const unsigned fl = ZS ? __ldcg(fw) : 0xffffffffu;
+  const unsigned u_maybe_nonzero = ZS ? __ldcg(tword) : 1u;
+  bool warp_zero = false;   // the whole warp's next operator input is zero
   float2 a[KP];
 
   if (G.do_inv) {
     // band tile V[b][k][l20 + ii] -> Xs[ii][k]
     for (int idx = tid; idx < TR * K; idx += NT) {
       const int k = idx / TR, i2 = idx % TR;
-      Xs[i2 * XP + k] = io.V[vbase + (long long)k * L2 + i2];
+      Xs[i2 * XP + k] = __ldcg(io.V + vbase + (long long)k * L2 + i2);
     }
     // first state chunk in flight while the inverse DFT runs
     double2 cb[CH];
@@ -537,8 +569,8 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
       const bool live = active && ((fl >> q) & 1u);
-      cb[q] = live ? cp[q * R] : make_double2(0.0, 0.0);
-      db[q] = (MOM && live) ? dp[q * R] : make_float2(0.f, 0.f);
+      cb[q] = live ? __ldcg(cp + q * R) : make_double2(0.0, 0.0);
+      db[q] = (MOM && live) ? __ldcg(dp + q * R) : make_float2(0.f, 0.f);
     }
     __syncthreads();
     unsigned nfl = 0;
@@ -556,7 +588,24 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
 #pragma unroll
       for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
       reg_dft<KP, true>(a);
-      // ---- fused epilogue, register-pipelined state stream
+      // ---- fused epilogue, register-pipelined state stream.
+      // Warp-level fast path: a clear segment whose 32 points all stay below the threshold
+      // stays exactly zero (same test as the per-point fast path below).  One warp AND-reduce
+      // covers all KP segments; when every segment qualifies the loop is skipped.
+      unsigned fast = 0u;
+      if constexpr (ZS) {
+        unsigned pass = 0u;
+#pragma unroll
+        for (int r = 0; r < KP; ++r) pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+        if (!active) pass = 0xffffffffu;
+        fast = __reduce_and_sync(0xffffffffu, pass) & ~fl;
+      }
+      constexpr unsigned ALL = KP >= 32 ? 0xffffffffu : ((1u << KP) - 1u);
+      if (ZS && (fast & ALL) == ALL) {
+#pragma unroll
+        for (int r = 0; r < KP; ++r) a[r] = make_float2(0.f, 0.f);
+        warp_zero = true;
+      } else
 #pragma unroll
       for (int r0 = 0; r0 < KP; r0 += CH) {
         double2 cn[CH];
@@ -565,17 +614,15 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
             const bool live = active && ((fl >> (r0 + CH + q)) & 1u);
-            cn[q] = live ? cp[(r0 + CH + q) * R] : make_double2(0.0, 0.0);
-            dn[q] = (MOM && live) ? dp[(r0 + CH + q) * R] : make_float2(0.f, 0.f);
+            cn[q] = live ? __ldcg(cp + (r0 + CH + q) * R) : make_double2(0.0, 0.0);
+            dn[q] = (MOM && live) ? __ldcg(dp + (r0 + CH + q) * R) : make_float2(0.f, 0.f);
           }
         }
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
           const int r = r0 + q;
           const float2 g = a[r];
-          // Warp-level fast path: a clear segment whose 32 points all stay below the threshold
-          // stays exactly zero (same test as the per-point fast path below).
-          if (ZS && !((fl >> r) & 1u) && __all_sync(0xffffffffu, fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
+          if (ZS && ((fast >> r) & 1u)) {
             a[r] = make_float2(0.f, 0.f);
             continue;
           }
@@ -626,9 +673,9 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
         a[r] = make_float2(0.f, 0.f);
         continue;
       }
-      double2 cc = cp[r * R];
+      double2 cc = __ldcg(cp + r * R);
       if (MOM) {
-        const float2 dd = dp[r * R];
+        const float2 dd = __ldcg(dp + r * R);
         cc.x = __fma_rn(bc, (double)dd.x, cc.x);
         cc.y = __fma_rn(bc, (double)dd.y, cc.y);
       }
@@ -642,13 +689,24 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   __shared__ unsigned live_rows[(TR + 31) / 32];
   if (tid < (TR + 31) / 32) live_rows[tid] = 0u;
   __syncthreads();
-  {
-    bool nzx = false;
+  bool nzx = false;
+  if (!warp_zero) {
 #pragma unroll
     for (int r = 0; r < KP; ++r) nzx |= (a[r].x != 0.f) | (a[r].y != 0.f);
     if (active && nzx) atomicOr(&live_rows[ii >> 5], 1u << (ii & 31));
   }
-  __syncthreads();
+  const bool tile_live = __syncthreads_or(active && nzx);
+  if (ZS && !tile_live) {
+    // the whole tile's next operator input is zero, so is its band: store zeros unless U
+    // already holds them from the previous step
+    if (u_maybe_nonzero) {
+      for (int idx = tid; idx < TR * K; idx += NT) {
+        const int k = idx / TR, i2 = idx % TR;
+        if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = make_float2(0.f, 0.f);
+      }
+      if (tid == 0) *tword = 0u;
+    }
+  } else {
   const bool my_live = (live_rows[ii >> 5] >> (ii & 31)) & 1u;
   if (active && my_live) {
     reg_dft<KP, false>(a);
@@ -681,6 +739,8 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
     const int k = idx / TR, i2 = idx % TR;
     if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
   }
+  if (ZS && tid == 0 && !u_maybe_nonzero) *tword = 1u;
+  }
   if constexpr (KP2 > 0) {
     __shared__ int s_last;
     __threadfence();                       // publish this CTA's U tile
@@ -691,7 +751,85 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
       __threadfence();                     // acquire the other CTAs' U tiles
       for (int l0 = 0; l0 < fc.K1; l0 += fc.TRc)
         cols_block<KP2>(fc.G, fc.ax, fc.io, (long long)b * fc.K1 + l0, fc.TRc, Xs);
+      if (done) {
+        __syncthreads();                   // every thread's V stores precede the release
+        if (tid == 0) {
+          __threadfence();
+          st_release_gpu(done + b, step + 1);
+        }
+      }
     }
+  }
+}
+
+template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0, int MINB = 2>
+__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
+    rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
+                           FusedCols fc) {
+  using TS = TileShape<KP, R, MO>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* Xs = reinterpret_cast<float2*>(smem_raw);
+  const float2* tw1s;
+  const float2* tw2s;
+  stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
+  fista_rows_tile<KP, R, MO, MOM, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs, nullptr, 0);
+}
+
+// Persistent dataflow solver for the fused-column shapes (config 2): one launch runs all
+// T + 1 steps.  Work items (step j, snapshot b, tile) are handed out in order by an atomic
+// queue; a step-j tile of snapshot b waits (acquire) until the column pass of step j - 1 of b
+// has published done[b] >= j.  Every item a CTA waits on was taken earlier by a running CTA,
+// so the wait chain always ends at an item with nothing to wait for (no co-residency
+// assumption).  Snapshots at different steps overlap, so there are no per-step kernel
+// boundaries, drains or wave tails; the twiddles are staged in shared memory once.
+struct PersistArgs {
+  Geo G;
+  AxisT<float2> ax;
+  RowsIO<float2> io;
+  EpiFista epi;
+  unsigned* flags;
+  FusedCols fc;
+  const double* beta;    // [t_end + 1]
+  int* queue;            // work-item counter (zeroed before the launch)
+  int* done;             // [B] column passes completed (zeroed before the launch)
+  int tiles_per_snap, batch, first_iteration, iterations;
+  int tw_off;            // float2 offset of the staged twiddles (past the rows and cols tiles)
+};
+
+template <int KP, int R, int MO, bool MOM, int KP2, int MINB>
+__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB) fista_persistent_kernel(PersistArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* Xs = reinterpret_cast<float2*>(smem_raw);
+  const float2* tw1s;
+  const float2* tw2s;
+  stage_twiddles<KP, R, MO>(A.ax, Xs + A.tw_off, tw1s, tw2s);
+  __shared__ int s_item[2];
+  const int per_step = A.batch * A.tiles_per_snap;
+  const int total = (A.iterations + 1) * per_step;
+  const int tid = threadIdx.x;
+  for (int n = 0;; n ^= 1) {
+    if (tid == 0) s_item[n] = atomicAdd(A.queue, 1);
+    __syncthreads();
+    const int item = s_item[n];
+    if (item >= total) break;
+    const int j = item / per_step, rem = item - j * per_step;
+    const int b = rem / A.tiles_per_snap;
+    const int t = A.first_iteration - 1 + j;
+    Geo G = A.G;
+    G.do_inv = j > 0;
+    G.do_fwd = j < A.iterations;
+    if (G.do_inv) {
+      if (tid == 0) {
+        while (ld_acquire_gpu(A.done + b) < j) __nanosleep(64);
+        __threadfence();
+      }
+      __syncthreads();
+    }
+    EpiFista e = A.epi;
+    e.it = t;
+    e.beta_cur = MOM ? A.beta[G.do_inv ? t : A.first_iteration] : 0.0;
+    e.beta_next = MOM ? A.beta[t + 1] : 0.0;
+    fista_rows_tile<KP, R, MO, MOM, true, KP2>(G, A.ax, A.io, e, A.flags, A.fc, rem, tw1s, tw2s, Xs, A.done, j);
   }
 }
 
@@ -739,7 +877,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
   const double kap2 = kap * kap;
   const double a_id = epi.a;
   unsigned* fw = ZS ? flags + ((long long)blockIdx.x * (NT / 32) + (tid >> 5)) : nullptr;
-  const unsigned fl = ZS ? *fw : 0xffffffffu;
+  const unsigned fl = ZS ? __ldcg(fw) : 0xffffffffu;
   double2 a[KP];
 
   // The dense dual v streams through shared memory: all KP values of a thread are requested
@@ -1164,7 +1302,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G,
   const int ii = tid / R, s = tid % R;
   const int gr = blockIdx.x * TR + ii;
   if (gr >= (int)G.rows) return;
-  const unsigned fl = flags[(long long)blockIdx.x * (NT / 32) + (tid >> 5)];
+  const unsigned fl = flags[(long long)blockIdx.x * (NT / 32 + 1) + (tid >> 5)];   // fista_rows_tile layout
   double2* cp = c + (long long)gr * G.L1 + s;
   float2* dp = d ? d + (long long)gr * G.L1 + s : nullptr;
 #pragma unroll
