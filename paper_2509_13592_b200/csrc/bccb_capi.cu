@@ -451,6 +451,8 @@ struct Workspace {
   unsigned char* flags;  // zero-segment flags of the streaming FISTA pass
   int* counters;         // [batch] arrival counters of the fused column pass, then [batch]
                          // column passes done and the work queue of the persistent solver
+  void* vs;              // [batch][K1][K2] complex128: spectral part of the ADMM dual
+  void* cb;              // [batch][K1][K2] complex128: last column-pass box of the split ADMM
 };
 
 // Rows engine of the specialised FISTA pass: the KP = 16 axis at 3 CTAs / SM for the shapes
@@ -485,7 +487,7 @@ static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R, int extra_w
 }
 
 // flags of the specialised FISTA rows pass (complex64 axis): per tile, one word per warp and
-// one tile word (fista_rows_tile)
+// one tile word (rows_tile)
 static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) {
   return flag_bytes_for(p, batch, rows_axis(p->ax1).R, 1);
 }
@@ -498,7 +500,7 @@ static size_t ws_bytes(const bccb_plan_s* p, int batch) {
   const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
   return 2 * align_up(inter) + 2 * align_up(box) +
          align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch))) +
-         align_up((size_t)(2 * batch + 32) * sizeof(int));
+         align_up((size_t)(2 * batch + 32) * sizeof(int)) + 2 * align_up((size_t)batch * box);
 }
 
 static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
@@ -517,6 +519,10 @@ static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   w.flags = (unsigned char*)ptr;
   ptr += align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch)));
   w.counters = (int*)ptr;
+  ptr += align_up((size_t)(2 * batch + 32) * sizeof(int));
+  w.vs = ptr;
+  ptr += align_up((size_t)batch * p->ax1.K * p->ax2.K * sizeof(double2));
+  w.cb = ptr;
   return w;
 }
 
@@ -883,7 +889,8 @@ static int launch_zero_segments_z(const bccb_plan_s* p, int batch, const Workspa
   return fail(BCCB_ERR_UNSUPPORTED, "no ADMM specialisation for this line shape");
 }
 
-static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace& w, double2* c, float2* d,
+template <typename T2>
+static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace& w, double2* c, T2* d,
                                 cudaStream_t st) {
   LaunchShape sh = fast_shape(p);
   const Geo G = rows_geo(p, batch, sh, false, false);
@@ -891,13 +898,13 @@ static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   const unsigned* fl = (const unsigned*)w.flags;
   if (rows_use_kp16(p->ax1)) {
-    if (p->ax1.s.R == 16) return launch_pass<float2>(zero_segments_kernel<16, 16>, KIND_OTHER, grid, sh, st, G, c, d, fl);
-    if (p->ax1.s.R == 64) return launch_pass<float2>(zero_segments_kernel<16, 64>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (p->ax1.s.R == 16) return launch_pass<float2>(zero_segments_kernel<16, 16, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (p->ax1.s.R == 64) return launch_pass<float2>(zero_segments_kernel<16, 64, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
   }
   const int key = fast_key(p->ax1.f);
 #define ZERO_CASE(KP_, R_, MO_)                                                                           \
   if (key == KP_ * 100000 + R_ * 10 + MO_)                                                                \
-    return launch_pass<float2>(zero_segments_kernel<KP_, R_>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    return launch_pass<float2>(zero_segments_kernel<KP_, R_, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
   FAST_SHAPES(ZERO_CASE)
 #undef ZERO_CASE
   return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
@@ -1526,6 +1533,147 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   return BCCB_OK;
 }
 
+// ---- ADMM with the spectral dual split (complex64 band engine; see EpiAdmmSplit)
+static bool admm_split_supported(const bccb_plan_s* p, int batch, const void* extra) {
+  static const int env = [] {
+    const char* e = getenv("BCCB_ADMM_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return env && fast_supported(p, batch, extra);
+}
+
+static int launch_rows_admm_split(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
+                                  const EpiAdmmSplit& e, cudaStream_t st) {
+  const LaunchShape sh = fast_shape(p);
+  const Geo G = rows_geo(p, batch, sh, inv, fwd);
+  RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  unsigned* fl = (unsigned*)w.flags;
+  if (rows_use_kp16(p->ax1)) {
+    const AxisT<float2> axs = p->ax1.dev_s();
+    const int k16 = fast_key(p->ax1.s);
+    if (k16 == 16 * 100000 + 16 * 10 + 2)
+      return launch_pass<float2>(rows_admm_split_kernel<16, 16, 2, 3>, KIND_ROWS, grid, sh, st, G, axs, io, e, fl);
+    if (k16 == 16 * 100000 + 64 * 10 + 4)
+      return launch_pass<float2>(rows_admm_split_kernel<16, 64, 4, 3>, KIND_ROWS, grid, sh, st, G, axs, io, e, fl);
+  }
+  const AxisT<float2> ax = p->ax1.dev<float2>();
+  const int key = fast_key(p->ax1.f);
+#define SPLIT_CASE(KP_, R_, MO_)                                                                             \
+  if (key == KP_ * 100000 + R_ * 10 + MO_)                                                                  \
+    return launch_pass<float2>(rows_admm_split_kernel<KP_, R_, MO_>, KIND_ROWS, grid, sh, st, G, ax, io, e, fl);
+  FAST_SHAPES(SPLIT_CASE)
+#undef SPLIT_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
+}
+
+static Geo cols_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool fwd, bool inv) {
+  Geo G;
+  G.L1 = p->L1;
+  G.L2 = p->L2;
+  G.rows = (long long)batch * p->ax1.K;
+  G.TR = sh.TR;
+  G.do_fwd = fwd ? 1 : 0;
+  G.do_inv = inv ? 1 : 0;
+  return G;
+}
+
+static int launch_cols_admm_split(const bccb_plan_s* p, int batch, const Workspace& w, const AdmmSplitBand& op,
+                                  cudaStream_t st) {
+  const LaunchShape sh = shape_for_prec(p->ax2, p->ax2.s, sizeof(float2), (long long)batch * p->ax1.K);
+  const Geo G = cols_geo(p, batch, sh, true, true);
+  ColsIO<float2> io{};
+  io.U = (const float2*)w.U;
+  io.V = (float2*)w.V;
+  io.K1 = p->ax1.K;
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const AxisT<float2> ax = p->ax2.dev_s();
+  KP_DISPATCH_F(ax.KP, return launch_pass<float2>(cols_admm_split_kernel<KPC>, KIND_COLS, grid, sh, st, G, ax, io, op));
+  return BCCB_OK;
+}
+
+// complex128 synthesis of a box: V = IFFT_col(box) (first half of IFFT2u(box))
+static int launch_cols_box_z(const bccb_plan_s* p, int batch, const Workspace& w, const double2* box,
+                             cudaStream_t st) {
+  const LaunchShape sh = shape_for<double2>(p->ax2, (long long)batch * p->ax1.K);
+  const Geo G = cols_geo(p, batch, sh, false, true);
+  ColsIO<double2> io{};
+  io.V = (double2*)w.V;
+  io.K1 = p->ax1.K;
+  const BoxIn<double2> op{box, p->ax2.K};
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const AxisT<double2> ax = p->ax2.dev<double2>();
+  KP_DISPATCH_D(ax.KP, return launch_pass<double2>(cols_box_kernel<KPC, double2>, KIND_COLS, grid, sh, st, G, ax, io, op));
+  return BCCB_OK;
+}
+
+// out = alpha (x1 - x2) + IFFT_row(V)  (complex128 engine)
+static int launch_rows_combine_z(const bccb_plan_s* p, int batch, const Workspace& w, const EpiCombine& e,
+                                 cudaStream_t st) {
+  const LaunchShape sh = shape_for<double2>(p->ax1);
+  const Geo G = rows_geo(p, batch, sh, true, false);
+  RowsIO<double2> io{(const double2*)w.V, (double2*)w.U};
+  const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  const AxisT<double2> ax = p->ax1.dev<double2>();
+  KP_DISPATCH_D(ax.KP, return launch_pass<double2>(rows_vector_kernel<KPC, double2, EpiCombine>, KIND_ROWS, grid, sh, st,
+                                                   G, ax, io, e));
+  return BCCB_OK;
+}
+
+// The split iteration (EpiAdmmSplit): the dual v is held as r (spatial, in the caller's v
+// buffer) + IFFT2u(vs) (box, workspace).  On entry r = v, vs = 0; on exit v = r + IFFT2u(vs)
+// and, when requested, c of the last iteration = a (z - r) + IFFT2u(Cb) from the pre-update
+// state.  Arithmetic of the rows / column passes: complex64 band FFTs, float64 state and box.
+static int admm_run_split(bccb_plan_s* p, int batch, int first_iteration, int iterations, double rho, double a,
+                          const double* tau, const float2* bhat, double2* z, double2* v, double2* c_last,
+                          int* first_bad, const Workspace& w, cudaStream_t st) {
+  int rc;
+  const size_t box_bytes = (size_t)batch * p->ax1.K * p->ax2.K * sizeof(double2);
+  CUDA_TRY(cudaMemsetAsync(w.vs, 0, box_bytes, st));
+  CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes(p, batch), st));
+  EpiAdmmSplit e;
+  e.z = z;
+  e.r = v;
+  e.tau = tau;
+  e.first_bad = first_bad;
+  e.a = a;
+  e.kscale = rho;
+  e.it = first_iteration;
+  AdmmSplitBand op;
+  op.D = (const double2*)w.D;
+  op.P = (const double2*)w.P;
+  op.Bh = bhat;
+  op.vs = (double2*)w.vs;
+  op.cb_out = nullptr;
+  op.rhoL = rho * (double)p->L1 * (double)p->L2;
+  op.K1 = p->ax1.K;
+  op.K2 = p->ax2.K;
+  const int t_end = first_iteration + iterations;
+  if ((rc = launch_rows_admm_split(p, batch, false, true, w, e, st))) return rc;
+  for (int t = first_iteration; t < t_end; ++t) {
+    const bool last = t + 1 == t_end;
+    op.cb_out = (last && c_last) ? (double2*)w.cb : nullptr;
+    if ((rc = launch_cols_admm_split(p, batch, w, op, st))) return rc;
+    if (last && c_last) {
+      // c = a (z - r) + IFFT2u(Cb) from the state before the last update; the complex128
+      // synthesis runs through U (free: the last rows pass has no forward half)
+      if ((rc = launch_zero_segments(p, batch, w, z, v, st))) return rc;
+      Workspace wu = w;
+      wu.V = w.U;
+      if ((rc = launch_cols_box_z(p, batch, wu, (const double2*)w.cb, st))) return rc;
+      const EpiCombine ec{z, v, c_last, a};
+      if ((rc = launch_rows_combine_z(p, batch, wu, ec, st))) return rc;
+    }
+    e.it = t;
+    if ((rc = launch_rows_admm_split(p, batch, true, !last, w, e, st))) return rc;
+  }
+  if ((rc = launch_zero_segments(p, batch, w, z, v, st))) return rc;
+  // v = r + IFFT2u(vs)
+  if ((rc = launch_cols_box_z(p, batch, w, (const double2*)w.vs, st))) return rc;
+  const EpiCombine ev{v, nullptr, v, 1.0};
+  return launch_rows_combine_z(p, batch, w, ev, st);
+}
+
 extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int iterations,
                              double rho, const double* tau,
                              const void* bhat_box, const void* extra, void* z, void* v, void* c_last,
@@ -1556,6 +1704,9 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
   e.extra_scale = 1.0 / (lo + rho);
   e.it = first_iteration;
   const int t_end = first_iteration + iterations;
+  if (admm_split_supported(p, batch, extra))
+    return admm_run_split(p, batch, first_iteration, iterations, rho, a, tau, (const float2*)bhat_box, (double2*)z,
+                          (double2*)v, (double2*)c_last, first_bad, w, st);
   // specialised shapes: zero-segment skipping on the sparse z (dual v is dense)
   const bool zs = admm_fast_supported(p, batch, extra);
   if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes_d(p, batch), st));

@@ -14,6 +14,8 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "band_fft.cuh"
 
 namespace bccb {
@@ -230,12 +232,16 @@ struct ColsIO {
   int K1;
 };
 
+// Default band stage of the column pass: Y = D*X + P*Bh from ColsIO.
+struct BandMulAdd {};
+
 // Column lines [row0, row0 + TR) (line = (snapshot b, column k1): length L2, band K2) processed
 // by one CTA of TR * ax.R threads (threads beyond that idle).  Shared by cols_kernel and the
 // fused rows kernel.  smem: TR x (K+1) band tile + TR x KP x pitch transpose buffer.
-template <int KP, typename C, bool U_GLOBAL = true>
+// Op (other than BandMulAdd) replaces the band stage: y = op(line, o, X or 0).
+template <int KP, typename C, bool U_GLOBAL = true, typename Op = BandMulAdd>
 __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, const ColsIO<C>& io, long long row0,
-                                           int TR, C* smem) {
+                                           int TR, C* smem, const Op& op = Op{}) {
   const int R = ax.R, K = ax.K, N = ax.N;
   const int XP = K + 1, SP = KP * ax.pitch;
   const int nthr = TR * R;
@@ -261,16 +267,20 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     const int i2 = idx / K, o = idx - i2 * K;
     const long long g2 = row0 + i2;
     if (g2 >= G.rows) continue;
-    const long long k1 = g2 % io.K1;
     C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
-    if (G.do_fwd) {
-      y = band_fwd_output(S + i2 * SP, o, KP, ax);
-      if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
-    }
-    if (io.Bh) {
-      C bh = to_c(io.Bh[g2 * K + o], C{});
-      if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
-      y = cadd(y, bh);
+    if constexpr (std::is_same<Op, BandMulAdd>::value) {
+      const long long k1 = g2 % io.K1;
+      if (G.do_fwd) {
+        y = band_fwd_output(S + i2 * SP, o, KP, ax);
+        if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
+      }
+      if (io.Bh) {
+        C bh = to_c(io.Bh[g2 * K + o], C{});
+        if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
+        y = cadd(y, bh);
+      }
+    } else {
+      y = op(g2, o, G.do_fwd ? band_fwd_output(S + i2 * SP, o, KP, ax) : y);
     }
     Xs[i2 * XP + o] = y;
   }
@@ -299,8 +309,8 @@ __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT
 
 // ------------------------------------------------------------------ pass A kernels
 // Generic pass A for plain-vector epilogues.
-template <int KP, typename C>
-__global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, AxisT<C> ax, RowsIO<C> io, EpiVector<C> epi) {
+template <int KP, typename C, typename E = EpiVector<C>>
+__global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, AxisT<C> ax, RowsIO<C> io, E epi) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int R = ax.R, K = ax.K;
@@ -326,7 +336,8 @@ __global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, AxisT<C> ax, Ro
       a[r] = G.do_inv ? epi.update(pos, b, a[r]) : epi.load(pos, b);
       mx = fmaxf(mx, (float)sqrt((double)a[r].x * a[r].x + (double)a[r].y * a[r].y));
     }
-    if (G.do_inv && epi.maxabs) group_atomic_max(epi.maxabs, b, mx);
+    if constexpr (std::is_same<E, EpiVector<C>>::value)
+      if (G.do_inv && epi.maxabs) group_atomic_max(epi.maxabs, b, mx);
   }
   if (G.do_fwd) {
     if (G.do_inv) __syncthreads();
@@ -516,37 +527,172 @@ __device__ __forceinline__ void stage_twiddles(const AxisT<float2>& ax, float2* 
   }
 }
 
-// One tile (TR lines of one snapshot) of the specialised FISTA rows pass.  `tile` indexes the
-// tile (and its flag words); with KP2 > 0 and do_fwd, the last tile of a snapshot to arrive
-// runs that snapshot's column pass and, in the persistent solver (done != null), publishes
-// `done[b] = step + 1`.  Streaming state / band loads bypass L1 (ld.global.cg): in the
-// persistent solver another SM wrote them in an earlier step.
-template <int KP, int R, int MO, bool MOM, bool ZS, int KP2>
-__device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
-                                                const EpiFista& epi, unsigned* __restrict__ flags,
-                                                const FusedCols& fc, int tile, const float2* tw1s,
-                                                const float2* tw2s, float2* Xs, int* done, int step) {
+// State policies of the specialised rows tile.  A policy is built per tile (state offset of
+// the thread's first point, snapshot b) and defines the per-point state S, its loads and
+// stores, the exact float64 update (out of line: only points with a nonzero state or |g| near
+// the threshold take it) and the next operator input.  A zero state with fp32 |g|^2 below
+// kappa^2 (1 - 2^-18) must stay exactly zero under the update (the zero fast path).
+template <bool MOM>
+struct FistaPolicy {
+  using Args = EpiFista;
+  struct S {
+    double2 c;
+    float2 d;
+  };
+  double2* cp;
+  float2* dp;
+  FistaScalars sc;
+  float bn;
+  __device__ __forceinline__ FistaPolicy(const EpiFista& e, long long off, int b) {
+    cp = e.c + off;
+    dp = MOM ? e.d + off : nullptr;
+    sc = FistaScalars{e.kscale * e.tau[b], e.a, e.beta_cur, b, e.it, e.first_bad};
+    bn = (float)e.beta_next;
+  }
+  __device__ __forceinline__ double kap() const { return sc.kap; }
+  __device__ __forceinline__ S load(int o, bool live) const {
+    S s;
+    s.c = live ? __ldcg(cp + o) : make_double2(0.0, 0.0);
+    s.d = (MOM && live) ? __ldcg(dp + o) : make_float2(0.f, 0.f);
+    return s;
+  }
+  __device__ __forceinline__ static bool zero(const S& s) {
+    return (s.c.x == 0.0) & (s.c.y == 0.0) & (!MOM | ((s.d.x == 0.f) & (s.d.y == 0.f)));
+  }
+  __device__ __forceinline__ static S empty() { return S{make_double2(0.0, 0.0), make_float2(0.f, 0.f)}; }
+  __device__ __forceinline__ S update(const S& s, float2 g) const {
+    S n = empty();
+    n.c = fista_point_slow<MOM>(s.c, s.d, g, sc, &n.d);
+    return n;
+  }
+  __device__ __forceinline__ void store(int o, const S& n) const {
+    cp[o] = n.c;
+    if (MOM) dp[o] = n.d;
+  }
+  // x_{t+1} = c_{t+1} + beta_{t+1} d_{t+1}
+  __device__ __forceinline__ float2 next_x(const S& n) const {
+    return MOM ? make_float2(fmaf(bn, n.d.x, (float)n.c.x), fmaf(bn, n.d.y, (float)n.c.y))
+               : make_float2((float)n.c.x, (float)n.c.y);
+  }
+  // x_t = c_t + beta_t d_t (first pass of a run)
+  __device__ __forceinline__ float2 first_x(const S& s) const {
+    double2 cc = s.c;
+    if (MOM) {
+      cc.x = __fma_rn(sc.bc, (double)s.d.x, cc.x);
+      cc.y = __fma_rn(sc.bc, (double)s.d.y, cc.y);
+    }
+    return make_float2((float)cc.x, (float)cc.y);
+  }
+};
+
+// ADMM with the dual split into a spatial part r and a spectral box part vs:
+// v = r + IFFT2u(vs).  The column pass accumulates vs in float64 on the box
+// (vs' = vs + Cb, Cb = D FFT2(w) + P Bhat - rho/(lam+rho) vs, w = z - r), so the part of the
+// dual that grows with t (SURVEY finding 7) never enters a spatial sum; the rows pass sees
+// V = IFFT2u(vs') and forms
+//   s = a w + r + IFFT2u(vs')   (= c + v),   z' = S_kappa(s),   r' = r + a w - z'
+// and the next operator input w' = z' - r'.  reference: pkg/src/bccblasso/solvers.py:403-436.
+struct EpiAdmmSplit {
+  double2* z;
+  double2* r;
+  const double* __restrict__ tau;  // [B]
+  int* first_bad;                  // [B]
+  double a, kscale;
+  int it;
+};
+
+__device__ __noinline__ void admm_split_point_slow(double2 z, double2 r, float2 g, double a, double kap,
+                                                   int* first_bad, int it, double2* zn, double2* rn) {
+  const double wr = z.x - r.x, wi = z.y - r.y;
+  const double awr = a * wr, awi = a * wi;
+  const double sr = (awr + r.x) + (double)g.x, si = (awi + r.y) + (double)g.y;
+  if (!isfinite(sr + si)) atomicMin(first_bad, it);
+  const double m2 = sr * sr + si * si;
+  double nr = 0.0, ni = 0.0;
+  if (!(m2 <= kap * kap)) {
+    const double f = 1.0 - kap * rsqrt(m2);
+    nr = sr * f;
+    ni = si * f;
+  }
+  *zn = make_double2(nr, ni);
+  *rn = make_double2((r.x + awr) - nr, (r.y + awi) - ni);
+}
+
+struct AdmmSplitPolicy {
+  using Args = EpiAdmmSplit;
+  struct S {
+    double2 z, r;
+  };
+  double2* zp;
+  double2* rp;
+  double a, kp;
+  int* fb;
+  int it;
+  __device__ __forceinline__ AdmmSplitPolicy(const EpiAdmmSplit& e, long long off, int b) {
+    zp = e.z + off;
+    rp = e.r + off;
+    a = e.a;
+    kp = e.kscale * e.tau[b];
+    fb = e.first_bad + b;
+    it = e.it;
+  }
+  __device__ __forceinline__ double kap() const { return kp; }
+  __device__ __forceinline__ S load(int o, bool live) const {
+    S s;
+    s.z = live ? __ldcg(zp + o) : make_double2(0.0, 0.0);
+    s.r = live ? __ldcg(rp + o) : make_double2(0.0, 0.0);
+    return s;
+  }
+  __device__ __forceinline__ static bool zero(const S& s) {
+    return (s.z.x == 0.0) & (s.z.y == 0.0) & (s.r.x == 0.0) & (s.r.y == 0.0);
+  }
+  __device__ __forceinline__ static S empty() { return S{make_double2(0.0, 0.0), make_double2(0.0, 0.0)}; }
+  __device__ __forceinline__ S update(const S& s, float2 g) const {
+    S n;
+    admm_split_point_slow(s.z, s.r, g, a, kp, fb, it, &n.z, &n.r);
+    return n;
+  }
+  __device__ __forceinline__ void store(int o, const S& n) const {
+    zp[o] = n.z;
+    rp[o] = n.r;
+  }
+  __device__ __forceinline__ float2 next_x(const S& n) const {
+    return make_float2((float)(n.z.x - n.r.x), (float)(n.z.y - n.r.y));
+  }
+  __device__ __forceinline__ float2 first_x(const S& s) const {
+    return make_float2((float)(s.z.x - s.r.x), (float)(s.z.y - s.r.y));
+  }
+};
+
+// One tile (TR lines of one snapshot) of the specialised rows pass, complex64 band engine,
+// state policy Pol.  `tile` indexes the tile (and its flag words); with KP2 > 0 and do_fwd,
+// the last tile of a snapshot to arrive runs that snapshot's column pass and, in the
+// persistent solver (done != null), publishes `done[b] = step + 1`.  Streaming state / band
+// loads bypass L1 (ld.global.cg): in the persistent solver another SM wrote them in an
+// earlier step.
+template <int KP, int R, int MO, typename Pol, bool ZS, int KP2>
+__device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
+                                          const typename Pol::Args& epi, unsigned* __restrict__ flags,
+                                          const FusedCols& fc, int tile, const float2* tw1s, const float2* tw2s,
+                                          float2* Xs, int* done, int step) {
   using TS = TileShape<KP, R, MO>;
+  using St = typename Pol::S;
   constexpr int NT = TS::NT, TR = TS::TR, K = TS::K, XP = TS::XP, PITCH = TS::PITCH, SP = TS::SP;
   constexpr int CH = 2;
   static_assert(KP % CH == 0, "chunking");
   float2* S = Xs + TR * XP;
   const int tid = threadIdx.x;
   const int ii = tid / R, s = tid % R;
-  const int row0 = tile * TR;            // rows < 2^31 (host check)
+  const int row0 = tile * TR;                  // rows < 2^31 (host check)
   const int gr = row0 + ii;
   const bool active = gr < (int)G.rows;
   const int L2 = G.L2;
   const int b = row0 / L2;                     // whole CTA lies in one snapshot
   const int l20 = row0 - b * L2;
   const long long vbase = (long long)b * K * L2 + l20;   // io.V/U index of (k=0, ii=0)
-  double2* cp = epi.c + (long long)gr * G.L1 + s;
-  float2* dp = MOM ? epi.d + (long long)gr * G.L1 + s : nullptr;
-  const double kap = epi.kscale * epi.tau[b];
+  const Pol pol(epi, (long long)gr * G.L1 + s, b);
+  const double kap = pol.kap();
   const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
-  const double a_id = epi.a, bc = epi.beta_cur;
-  const float bn = (float)epi.beta_next;
-  const FistaScalars sc{kap, a_id, bc, b, epi.it, epi.first_bad};
   const int lane = tid & 31;
   // flag words per tile: NT/32 warp words (zero segments), then one tile word (bit 0: the
   // tile's U band may be nonzero; clear = U already holds zeros, the store can be skipped)
@@ -564,14 +710,9 @@ __device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2
       Xs[i2 * XP + k] = __ldcg(io.V + vbase + (long long)k * L2 + i2);
     }
     // first state chunk in flight while the inverse DFT runs
-    double2 cb[CH];
-    float2 db[CH];
+    St sb[CH];
 #pragma unroll
-    for (int q = 0; q < CH; ++q) {
-      const bool live = active && ((fl >> q) & 1u);
-      cb[q] = live ? __ldcg(cp + q * R) : make_double2(0.0, 0.0);
-      db[q] = (MOM && live) ? __ldcg(dp + q * R) : make_float2(0.f, 0.f);
-    }
+    for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
     __syncthreads();
     unsigned nfl = 0;
     {
@@ -608,15 +749,10 @@ __device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2
       } else
 #pragma unroll
       for (int r0 = 0; r0 < KP; r0 += CH) {
-        double2 cn[CH];
-        float2 dn[CH];
+        St sn[CH];
         if (r0 + CH < KP) {
 #pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const bool live = active && ((fl >> (r0 + CH + q)) & 1u);
-            cn[q] = live ? __ldcg(cp + (r0 + CH + q) * R) : make_double2(0.0, 0.0);
-            dn[q] = (MOM && live) ? __ldcg(dp + (r0 + CH + q) * R) : make_float2(0.f, 0.f);
-          }
+          for (int q = 0; q < CH; ++q) sn[q] = pol.load((r0 + CH + q) * R, active && ((fl >> (r0 + CH + q)) & 1u));
         }
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
@@ -626,42 +762,22 @@ __device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2
             a[r] = make_float2(0.f, 0.f);
             continue;
           }
-          const double2 cc = cb[q];
-          const float2 dd = db[q];
-          const bool zero_state = (cc.x == 0.0) & (cc.y == 0.0) & (!MOM | ((dd.x == 0.f) & (dd.y == 0.f)));
-          double nr = 0.0, ni = 0.0;
-          float2 dnew = make_float2(0.f, 0.f);
-          bool nz = false;
-          if (active && !(zero_state && fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
-            const double2 cn = fista_point_slow<MOM>(cc, dd, g, sc, &dnew);
-            nr = cn.x;
-            ni = cn.y;
-            nz = true;   // state touched: value may be nonzero or may have changed
-            if (!ZS) {
-              cp[r * R] = make_double2(nr, ni);
-              if (MOM) dp[r * R] = dnew;
-            }
+          St n = Pol::empty();
+          if (active && !(Pol::zero(sb[q]) && fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
+            n = pol.update(sb[q], g);
+            if (!ZS) pol.store(r * R, n);
           }
           if (ZS) {
-            const bool nzv = (nr != 0.0) | (ni != 0.0) | (MOM & ((dnew.x != 0.f) | (dnew.y != 0.f)));
-            if (__any_sync(0xffffffffu, nzv)) {  // segment (still / newly) nonzero: write it whole
-              if (active) {
-                cp[r * R] = make_double2(nr, ni);
-                if (MOM) dp[r * R] = dnew;
-              }
+            if (__any_sync(0xffffffffu, !Pol::zero(n))) {  // segment (still / newly) nonzero: write it whole
+              if (active) pol.store(r * R, n);
               nfl |= 1u << r;
             }
           }
-          (void)nz;
-          a[r] = MOM ? make_float2(fmaf(bn, dnew.x, (float)nr), fmaf(bn, dnew.y, (float)ni))
-                     : make_float2((float)nr, (float)ni);
+          a[r] = pol.next_x(n);
         }
         if (r0 + CH < KP) {
 #pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            cb[q] = cn[q];
-            db[q] = dn[q];
-          }
+          for (int q = 0; q < CH; ++q) sb[q] = sn[q];
         }
       }
     }
@@ -673,13 +789,7 @@ __device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2
         a[r] = make_float2(0.f, 0.f);
         continue;
       }
-      double2 cc = __ldcg(cp + r * R);
-      if (MOM) {
-        const float2 dd = __ldcg(dp + r * R);
-        cc.x = __fma_rn(bc, (double)dd.x, cc.x);
-        cc.y = __fma_rn(bc, (double)dd.y, cc.y);
-      }
-      a[r] = make_float2((float)cc.x, (float)cc.y);
+      a[r] = pol.first_x(pol.load(r * R, true));
     }
   }
   if (!G.do_fwd) return;
@@ -707,39 +817,39 @@ __device__ __forceinline__ void fista_rows_tile(const Geo& G, const AxisT<float2
       if (tid == 0) *tword = 0u;
     }
   } else {
-  const bool my_live = (live_rows[ii >> 5] >> (ii & 31)) & 1u;
-  if (active && my_live) {
-    reg_dft<KP, false>(a);
-    float2* Srow = S + ii * SP;
+    const bool my_live = (live_rows[ii >> 5] >> (ii & 31)) & 1u;
+    if (active && my_live) {
+      reg_dft<KP, false>(a);
+      float2* Srow = S + ii * SP;
 #pragma unroll
-    for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], tw1s[j * R + s]);
-  }
-  __syncthreads();
-  for (int idx = tid; idx < TR * K; idx += NT) {
-    const int i2 = idx / K, o = idx % K;
-    if (!((live_rows[i2 >> 5] >> (i2 & 31)) & 1u)) {
-      Xs[i2 * XP + o] = make_float2(0.f, 0.f);
-      continue;
+      for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], tw1s[j * R + s]);
     }
-    const int j = o % KP, m = o / KP;
-    const float2* row = S + i2 * SP + j * PITCH;
-    float2 acc = make_float2(0.f, 0.f);
-    if (m == 0) {
+    __syncthreads();
+    for (int idx = tid; idx < TR * K; idx += NT) {
+      const int i2 = idx / K, o = idx % K;
+      if (!((live_rows[i2 >> 5] >> (i2 & 31)) & 1u)) {
+        Xs[i2 * XP + o] = make_float2(0.f, 0.f);
+        continue;
+      }
+      const int j = o % KP, m = o / KP;
+      const float2* row = S + i2 * SP + j * PITCH;
+      float2 acc = make_float2(0.f, 0.f);
+      if (m == 0) {
 #pragma unroll
-      for (int t = 0; t < R; ++t) acc = cadd(acc, row[t]);
-    } else {
-      const float2* tw = tw2s + m * R;
+        for (int t = 0; t < R; ++t) acc = cadd(acc, row[t]);
+      } else {
+        const float2* tw = tw2s + m * R;
 #pragma unroll
-      for (int t = 0; t < R; ++t) acc = cfma(row[t], tw[t], acc);
+        for (int t = 0; t < R; ++t) acc = cfma(row[t], tw[t], acc);
+      }
+      Xs[i2 * XP + o] = acc;
     }
-    Xs[i2 * XP + o] = acc;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < TR * K; idx += NT) {
-    const int k = idx / TR, i2 = idx % TR;
-    if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
-  }
-  if (ZS && tid == 0 && !u_maybe_nonzero) *tword = 1u;
+    __syncthreads();
+    for (int idx = tid; idx < TR * K; idx += NT) {
+      const int k = idx / TR, i2 = idx % TR;
+      if (row0 + i2 < (int)G.rows) io.U[vbase + (long long)k * L2 + i2] = Xs[i2 * XP + k];
+    }
+    if (ZS && tid == 0 && !u_maybe_nonzero) *tword = 1u;
   }
   if constexpr (KP2 > 0) {
     __shared__ int s_last;
@@ -772,7 +882,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
-  fista_rows_tile<KP, R, MO, MOM, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs, nullptr, 0);
+  rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs, nullptr, 0);
 }
 
 // Persistent dataflow solver for the fused-column shapes (config 2): one launch runs all
@@ -829,9 +939,102 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB) fista_p
     e.it = t;
     e.beta_cur = MOM ? A.beta[G.do_inv ? t : A.first_iteration] : 0.0;
     e.beta_next = MOM ? A.beta[t + 1] : 0.0;
-    fista_rows_tile<KP, R, MO, MOM, true, KP2>(G, A.ax, A.io, e, A.flags, A.fc, rem, tw1s, tw2s, Xs, A.done, j);
+    rows_tile<KP, R, MO, FistaPolicy<MOM>, true, KP2>(G, A.ax, A.io, e, A.flags, A.fc, rem, tw1s, tw2s, Xs, A.done, j);
   }
 }
+
+// ---------------------------------------------------------------- ADMM, spectral dual split
+// Rows pass of the split ADMM (AdmmSplitPolicy): complex64 band engine, zero-segment skipping on
+// the (z, r) state, which stays sparse because the growing part of the dual lives on the box.
+template <int KP, int R, int MO, int MINB = 2>
+__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
+    rows_admm_split_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiAdmmSplit epi,
+                           unsigned* __restrict__ flags) {
+  using TS = TileShape<KP, R, MO>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* Xs = reinterpret_cast<float2*>(smem_raw);
+  const float2* tw1s;
+  const float2* tw2s;
+  stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
+  const FusedCols nofc{};
+  rows_tile<KP, R, MO, AdmmSplitPolicy, true, 0>(G, ax, io, epi, flags, nofc, blockIdx.x, tw1s, tw2s, Xs, nullptr, 0);
+}
+
+// Band stage of the split ADMM column pass (float64 on the box):
+//   Cb = D X + P Bh - rho L P vs,   vs' = vs + Cb,   Y = vs'  (-> V = IFFT_col(vs'))
+// and, on the last iteration, Cb is kept for c = a w + IFFT2u(Cb).
+struct AdmmSplitBand {
+  const double2* __restrict__ D;   // [K1][K2]
+  const double2* __restrict__ P;   // [K1][K2]
+  const float2* __restrict__ Bh;   // [B][K1][K2]
+  double2* vs;                     // [B][K1][K2]
+  double2* cb_out;                 // [B][K1][K2] or null
+  double rhoL;
+  int K1, K2;
+  __device__ __forceinline__ float2 operator()(long long line, int o, float2 x) const {
+    const long long k1 = line % K1;
+    const long long bi = line * K2 + o;
+    const double2 d = __ldg(D + k1 * K2 + o), pp = __ldg(P + k1 * K2 + o);
+    const float2 bh = Bh[bi];
+    const double2 v = vs[bi];
+    const double xr = x.x, xi = x.y, br = bh.x, bim = bh.y;
+    const double rr = rhoL * pp.x, ri = rhoL * pp.y;
+    double cr = __fma_rn(d.x, xr, -d.y * xi) + __fma_rn(pp.x, br, -pp.y * bim);
+    double ci = __fma_rn(d.x, xi, d.y * xr) + __fma_rn(pp.x, bim, pp.y * br);
+    cr -= __fma_rn(rr, v.x, -ri * v.y);
+    ci -= __fma_rn(rr, v.y, ri * v.x);
+    const double2 vn = make_double2(v.x + cr, v.y + ci);
+    vs[bi] = vn;
+    if (cb_out) cb_out[bi] = make_double2(cr, ci);
+    return make_float2((float)vn.x, (float)vn.y);
+  }
+};
+
+template <int KP>
+__global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_admm_split_kernel(Geo G, AxisT<float2> ax,
+                                                                             ColsIO<float2> io, AdmmSplitBand op) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cols_block<KP, float2, true, AdmmSplitBand>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR,
+                                               reinterpret_cast<float2*>(smem_raw), op);
+}
+
+// Box input at engine precision for a synthesis column pass (y = box[line][o]).
+template <typename C>
+struct BoxIn {
+  const C* __restrict__ box;   // [B][K1][K2]
+  int K2;
+  __device__ __forceinline__ C operator()(long long line, int o, C) const { return box[line * K2 + o]; }
+};
+
+template <int KP, typename C>
+__global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_box_kernel(Geo G, AxisT<C> ax, ColsIO<C> io,
+                                                                      BoxIn<C> op) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cols_block<KP, C, true, BoxIn<C>>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR, reinterpret_cast<C*>(smem_raw),
+                                    op);
+}
+
+// Epilogue of the split-ADMM finalisation: out = alpha (x1 - x2) + g (c = a (z - r) + IFFT2u(Cb))
+// or, with x2 = null, out = x1 + g (v = r + IFFT2u(vs)).
+struct EpiCombine {
+  const double2* x1;
+  const double2* x2;
+  double2* out;
+  double alpha;
+  __device__ __forceinline__ double2 load(long long pos, int) const { return x1[pos]; }
+  __device__ __forceinline__ double2 update(long long pos, int, double2 g) const {
+    const double2 a1 = x1[pos];
+    double2 o;
+    if (x2) {
+      const double2 a2 = x2[pos];
+      o = make_double2(__fma_rn(alpha, a1.x - a2.x, g.x), __fma_rn(alpha, a1.y - a2.y, g.y));
+    } else {
+      o = make_double2(a1.x + g.x, a1.y + g.y);
+    }
+    out[pos] = o;
+    return o;
+  }
+};
 
 // cp.async (LDGSTS): per-thread asynchronous global -> shared copies that hold no registers
 // while in flight.
@@ -1293,8 +1496,8 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 1) cluster64_fi
 
 // Final pass of a zero-skipping run: write the zeros of every clear segment back so c (and d)
 // are dense, consistent arrays again.
-template <int KP, int R>
-__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G, double2* c, float2* d,
+template <int KP, int R, typename T2 = float2>
+__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G, double2* c, T2* d,
                                                                           const unsigned* __restrict__ flags) {
   constexpr int NT = R > 256 ? R : 256;
   constexpr int TR = NT / R;
@@ -1302,14 +1505,14 @@ __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G,
   const int ii = tid / R, s = tid % R;
   const int gr = blockIdx.x * TR + ii;
   if (gr >= (int)G.rows) return;
-  const unsigned fl = flags[(long long)blockIdx.x * (NT / 32 + 1) + (tid >> 5)];   // fista_rows_tile layout
+  const unsigned fl = flags[(long long)blockIdx.x * (NT / 32 + 1) + (tid >> 5)];   // rows_tile layout
   double2* cp = c + (long long)gr * G.L1 + s;
-  float2* dp = d ? d + (long long)gr * G.L1 + s : nullptr;
+  T2* dp = d ? d + (long long)gr * G.L1 + s : nullptr;
 #pragma unroll
   for (int r = 0; r < KP; ++r)
     if (!((fl >> r) & 1u)) {
       cp[r * R] = make_double2(0.0, 0.0);
-      if (dp) dp[r * R] = make_float2(0.f, 0.f);
+      if (dp) dp[r * R] = T2{};
     }
 }
 

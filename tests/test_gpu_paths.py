@@ -79,10 +79,13 @@ def test_ista_auto_vs_generic(cfg, nsnap, generic_path):
 
 
 def test_admm_auto_vs_generic_and_oracle(generic_path):
-    """Small threshold: z leaves zero, exercising the z-skipping kernel.  This regime is
-    ill-conditioned (points hover at the threshold: rounding b to complex64 moves the float64
-    answer by ~2e-3), so both sides get identical inputs: complex64 y, whose signed scatter
-    (the GPU's fft2(b) on the box) is exact."""
+    """Small threshold: z leaves zero, exercising the z / r skipping of the split-dual kernels
+    (the automatic path: complex64 band FFTs, dual growth on the float64 box) against the
+    generic complex128 engine and the oracle.  This regime is ill-conditioned (points hover at
+    the threshold: rounding b to complex64 moves the float64 answer by ~2e-3), so both sides
+    get identical inputs: complex64 y, whose signed scatter (the GPU's fft2(b) on the box) is
+    exact."""
+    from paper_2509_13592_b200.solvers import admm_solve_with_c
     w = scenes.workload(3)
     geom, ys, _ = scenes.make_scene(w, range(2))
     op = bb.gram_operator(geom, w.l1, w.l2)
@@ -93,12 +96,16 @@ def test_admm_auto_vs_generic_and_oracle(generic_path):
     conf = bb.SolverConfig(iterations=40, rho=1.0)
     auto = bb.admm_solve(bb.LassoProblem.from_measurements(op, y32, tau=taus), conf).estimate
     gen = generic_path(lambda: bb.admm_solve(bb.LassoProblem.from_measurements(op, y32, tau=taus), conf).estimate)
+    za, va, ca = (t.cpu().numpy() for t in admm_solve_with_c(bb.LassoProblem.from_measurements(op, y32, tau=taus), conf))
     eig = orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2)
     for i in range(2):
         z, c, v = orc.admm(eig, bs[i], taus[i], 1.0, 40)
         assert np.count_nonzero(z) > 0
-        assert orc.rel_l2(auto[i], gen[i]) < 1e-9
+        assert orc.rel_l2(auto[i], gen[i]) < 1e-6
         assert orc.rel_l2(auto[i], z) < 1e-6
+        np.testing.assert_array_equal(za[i], auto[i])
+        assert orc.rel_l2(ca[i], c) < 1e-6
+        assert orc.rel_l2(va[i], v) < 1e-6
 
 
 @pytest.mark.parametrize("m1,m2,l1,l2", [(6, 4, 9, 6), (5, 3, 12, 10), (4, 4, 20, 8), (3, 5, 7, 16)])
