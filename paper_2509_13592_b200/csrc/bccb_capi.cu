@@ -698,8 +698,8 @@ static LaunchShape fast_shape(const bccb_plan_s* p) {
   const int pitch = (a.R % 2 == 1) ? a.R : a.R + 1;
   // band tile + transpose buffer (+ staged twiddles [KP][R], [Mo][R] when <= 8 KB: STAGE_TW)
   const size_t tw = (size_t)(a.KP + a.Mo) * a.R;
-  sh.smem = ((size_t)sh.TR * (p->ax1.K + 1) + (size_t)sh.TR * a.KP * pitch + (tw * 8 <= 8192 ? tw : 0)) *
-            sizeof(float2);
+  sh.smem = ((size_t)sh.TR * (p->ax1.K + 2) + (size_t)sh.TR * a.KP * pitch + (tw * 8 <= 8192 ? tw : 0)) *
+            sizeof(float2);   // TileShape: band rows of K + 2
   return sh;
 }
 
@@ -1367,7 +1367,7 @@ static int launch_fista_persistent(bccb_plan_s* p, int batch, int first, int ite
   sh.TR = sh.threads / a.R;
   const int pitch = (a.R % 2 == 1) ? a.R : a.R + 1;
   const int pitch2 = (c.R % 2 == 1) ? c.R : c.R + 1;
-  const size_t rows_area = (size_t)sh.TR * (p->ax1.K + 1) + (size_t)sh.TR * a.KP * pitch;
+  const size_t rows_area = (size_t)sh.TR * (p->ax1.K + 2) + (size_t)sh.TR * a.KP * pitch;
   const size_t cols_area = (size_t)fc.TRc * (p->ax2.K + 1) + (size_t)fc.TRc * c.KP * pitch2;
   const size_t tw = (size_t)(a.KP + a.Mo) * a.R;
   PersistArgs A;

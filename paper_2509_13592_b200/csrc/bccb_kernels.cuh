@@ -505,7 +505,7 @@ struct TileShape {
   static constexpr int NT = R > 256 ? R : 256;   // threads per CTA
   static constexpr int TR = NT / R;              // lines per CTA
   static constexpr int K = KP * MO;
-  static constexpr int XP = K + 1;
+  static constexpr int XP = K + 2;   // even: 16-byte aligned band rows (LDS.128 pairs)
   static constexpr int PITCH = (R % 2 == 1) ? R : R + 1;
   static constexpr int SP = KP * PITCH;
   static constexpr bool STAGE_TW = (KP + MO) * R * 8 <= 8192;
@@ -702,6 +702,8 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   const unsigned u_maybe_nonzero = ZS ? __ldcg(tword) : 1u;
   bool warp_zero = false;   // the whole warp's next operator input is zero
   float2 a[KP];
+  __shared__ unsigned live_rows[(TR + 31) / 32];   // lines whose next operator input is nonzero
+  auto live_rows_zero = [&](int i) { live_rows[i] = 0u; };
 
   if (G.do_inv) {
     // band tile V[b][k][l20 + ii] -> Xs[ii][k]
@@ -713,18 +715,28 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     St sb[CH];
 #pragma unroll
     for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
+    if (G.do_fwd && tid < (TR + 31) / 32) live_rows_zero(tid);
     __syncthreads();
     unsigned nfl = 0;
     {
-      // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT)
-      const float2* Y = Xs + ii * XP;
+      // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT); the band row
+      // is read as 16-byte pairs
+      const float4* Y4 = reinterpret_cast<const float4*>(Xs + ii * XP);
 #pragma unroll
-      for (int j = 0; j < KP; ++j) a[j] = Y[j];
+      for (int j = 0; j < KP; j += 2) {
+        const float4 q = Y4[j / 2];
+        a[j] = make_float2(q.x, q.y);
+        a[j + 1] = make_float2(q.z, q.w);
+      }
 #pragma unroll
       for (int m = 1; m < MO; ++m) {
         const float2 w2 = tw2s[m * R + s];
 #pragma unroll
-        for (int j = 0; j < KP; ++j) a[j] = cadd(a[j], cmulc(Y[j + KP * m], w2));
+        for (int j = 0; j < KP; j += 2) {
+          const float4 q = Y4[(j + KP * m) / 2];
+          a[j] = cadd(a[j], cmulc(make_float2(q.x, q.y), w2));
+          a[j + 1] = cadd(a[j + 1], cmulc(make_float2(q.z, q.w), w2));
+        }
       }
 #pragma unroll
       for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
@@ -796,9 +808,10 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   // ---- band forward: register DFT, twiddle + transpose scatter, R-term reductions.
   // A line whose next operator input is entirely zero (most lines once the iterate is sparse)
   // has a zero band: its DFT, scatter and reductions are skipped.
-  __shared__ unsigned live_rows[(TR + 31) / 32];
-  if (tid < (TR + 31) / 32) live_rows[tid] = 0u;
-  __syncthreads();
+  if (!G.do_inv) {                        // (zeroed before the band-load barrier otherwise)
+    if (tid < (TR + 31) / 32) live_rows_zero(tid);
+    __syncthreads();
+  }
   bool nzx = false;
   if (!warp_zero) {
 #pragma unroll
