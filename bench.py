@@ -269,7 +269,7 @@ def main():
     ms_k = (ctypes.c_double * 3)()
     n_k = (ctypes.c_longlong * 3)()
     _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
-    _lib.check(_lib.lib.bccb_set_substreams(2))
+    _lib.check(_lib.lib.bccb_set_substreams(int(os.environ.get("BCCB_SUBSTREAMS", "2"))))
     rows_ms = ms_k[0] / max(n_k[0], 1)
     cols_ms = ms_k[1] / max(n_k[1], 1)
     step_kernel_ms = ms_k[0] + ms_k[1] + ms_k[2]

@@ -189,11 +189,12 @@ struct bccb_plan_s {
   int M = 0;                       // occupied elements (Gram plans)
   int* occ_dev = nullptr;          // [3][M]: m1, m2 (reduced mod L1 / L2), (m1 + m2) & 1
   int occ_alias = 0;               // some occupied cells alias (M1 > L1 or M2 > L2)
-  cudaStream_t aux = nullptr;      // second stream for the sub-batch split (created lazily)
+  static constexpr int MAX_SUB = 4;
+  cudaStream_t aux[MAX_SUB - 1] = {};   // extra streams of the sub-batch split (created lazily)
   double* beta_dev = nullptr;      // momentum table of the small-grid persistent solver
   size_t beta_cap = 0;
   std::vector<double> beta_host;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join[MAX_SUB - 1] = {};
   bool full() const { return ax1.K == L1 && ax2.K == L2; }
 };
 
@@ -279,10 +280,12 @@ static void free_plan(bccb_plan_s* p) {
   free_axis(p->ax2);
   cudaFree(p->lam_box_dev);
   cudaFree(p->occ_dev);
-  if (p->aux) cudaStreamDestroy(p->aux);
+  for (int i = 0; i < bccb_plan_s::MAX_SUB - 1; ++i) {
+    if (p->aux[i]) cudaStreamDestroy(p->aux[i]);
+    if (p->ev_join[i]) cudaEventDestroy(p->ev_join[i]);
+  }
   cudaFree(p->beta_dev);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-  if (p->ev_join) cudaEventDestroy(p->ev_join);
   cudaSetDevice(cur);
   delete p;
 }
@@ -1164,32 +1167,34 @@ static int check_singular_admm(const bccb_plan_s* p, double rho) {
   return BCCB_OK;
 }
 
-// Sub-batch split (BCCB_SUBSTREAMS=1 or bccb_set_substreams(1) disables): only when each half
-// still fills the GPU.
+// Sub-batch split into n streams (BCCB_SUBSTREAMS / bccb_set_substreams; 1 disables): only
+// while each part still fills the GPU (>= 2048 lines).
 static std::atomic<int> g_substreams{-1};
 
 extern "C" int bccb_set_substreams(int n) {
-  if (n < 1 || n > 2) return fail(BCCB_ERR_INVALID, "substreams must be 1 or 2");
+  if (n < 1 || n > bccb_plan_s::MAX_SUB) return fail(BCCB_ERR_INVALID, "substreams must be in [1, %d]", bccb_plan_s::MAX_SUB);
   g_substreams.store(n);
   return BCCB_OK;
 }
 
 static int sub_batches(const bccb_plan_s* p, int batch) {
-  int env = g_substreams.load();
-  if (env < 0) {
+  int n = g_substreams.load();
+  if (n < 0) {
     const char* e = getenv("BCCB_SUBSTREAMS");
-    env = e ? atoi(e) : 2;
+    n = e ? atoi(e) : 2;
   }
-  if (env < 2 || batch < 2) return 1;
-  const long long half_lines = (long long)(batch / 2) * p->L2;
-  return half_lines >= 2048 ? 2 : 1;
+  n = std::max(1, std::min(n, bccb_plan_s::MAX_SUB));
+  while (n > 1 && (batch < n || (long long)(batch / n) * p->L2 < 2048)) --n;
+  return n;
 }
 
-static int ensure_aux_stream(bccb_plan_s* p) {
-  if (p->aux) return BCCB_OK;
-  CUDA_TRY(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
-  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+static int ensure_aux_streams(bccb_plan_s* p, int n) {
+  if (!p->ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  for (int i = 0; i < n - 1; ++i) {
+    if (p->aux[i]) continue;
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming));
+  }
   return BCCB_OK;
 }
 
@@ -1462,18 +1467,18 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   // column pass and kernel tails overlap the other half's rows pass.  Snapshots are
   // independent, so the arithmetic is identical to one stream (bitwise).
   const int nsub = sub_batches(p, batch);
-  if (nsub > 1 && (rc = ensure_aux_stream(p))) return rc;
+  if (nsub > 1 && (rc = ensure_aux_streams(p, nsub))) return rc;
   struct Sub {
     int b0, nb;
     cudaStream_t st;
     Workspace w;
     EpiFista e;
-  } sub[2];
+  } sub[bccb_plan_s::MAX_SUB];
   for (int q = 0; q < nsub; ++q) {
     Sub& u = sub[q];
     u.b0 = (int)((long long)batch * q / nsub);
     u.nb = (int)((long long)batch * (q + 1) / nsub) - u.b0;
-    u.st = q == 0 ? st : p->aux;
+    u.st = q == 0 ? st : p->aux[q - 1];
     u.w = w;
     const long long inter = (long long)u.b0 * p->ax1.K * p->L2;
     u.w.U = (float2*)w.U + inter;
@@ -1492,7 +1497,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   }
   const float2* bh = (const float2*)bhat_box;
   const bool fuse = zs && fused_supported(p);
-  FusedCols fcs[2];
+  FusedCols fcs[bccb_plan_s::MAX_SUB];
   for (int q = 0; q < nsub && fuse; ++q)
     fcs[q] = make_fused(p, sub[q].nb, sub[q].w, (const float2*)w.D, (const float2*)w.P,
                         bh + (long long)sub[q].b0 * p->ax1.K * p->ax2.K);
@@ -1507,7 +1512,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   };
   if (nsub > 1) {
     CUDA_TRY(cudaEventRecord(p->ev_fork, st));
-    CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+    for (int q = 1; q < nsub; ++q) CUDA_TRY(cudaStreamWaitEvent(p->aux[q - 1], p->ev_fork, 0));
   }
   for (int q = 0; q < nsub; ++q)
     if ((rc = rows(q, false, true))) return rc;
@@ -1526,9 +1531,9 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   }
   for (int q = 0; q < nsub; ++q)
     if (zs && (rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].e.c, sub[q].e.d, sub[q].st))) return rc;
-  if (nsub > 1) {
-    CUDA_TRY(cudaEventRecord(p->ev_join, p->aux));
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
+  for (int q = 1; q < nsub; ++q) {
+    CUDA_TRY(cudaEventRecord(p->ev_join[q - 1], p->aux[q - 1]));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join[q - 1], 0));
   }
   return BCCB_OK;
 }
