@@ -452,8 +452,7 @@ struct Workspace {
   void* D;
   void* P;
   unsigned char* flags;  // zero-segment flags of the streaming FISTA pass
-  int* counters;         // [batch] arrival counters of the fused column pass, then [batch]
-                         // column passes done and the work queue of the persistent solver
+  int* counters;         // [batch] arrival counters of the fused column pass
   void* vs;              // [batch][K1][K2] complex128: spectral part of the ADMM dual
   void* cb;              // [batch][K1][K2] complex128: last column-pass box of the split ADMM
 };
@@ -503,7 +502,7 @@ static size_t ws_bytes(const bccb_plan_s* p, int batch) {
   const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
   return 2 * align_up(inter) + 2 * align_up(box) +
          align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch))) +
-         align_up((size_t)(2 * batch + 32) * sizeof(int)) + 2 * align_up((size_t)batch * box);
+         align_up((size_t)batch * sizeof(int)) + 2 * align_up((size_t)batch * box);
 }
 
 static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
@@ -522,7 +521,7 @@ static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   w.flags = (unsigned char*)ptr;
   ptr += align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch)));
   w.counters = (int*)ptr;
-  ptr += align_up((size_t)(2 * batch + 32) * sizeof(int));
+  ptr += align_up((size_t)batch * sizeof(int));
   w.vs = ptr;
   ptr += align_up((size_t)batch * p->ax1.K * p->ax2.K * sizeof(double2));
   w.cb = ptr;
@@ -714,10 +713,9 @@ static LaunchShape fast_shape(const bccb_plan_s* p) {
   X(16, 16, 2, 16, 3) /* config 2, KP 16 engine */ \
   X(16, 16, 2, 16, 4) /* same, 4 CTAs/SM (BCCB_FUSED_MINB=4) */
 
-// `ratio`: largest (column work of a snapshot) / (rows work of a CTA) accepted.  The per-pass
-// kernel takes 1 (the last CTA's column tail must not dominate); the persistent solver takes 4
-// (other snapshots' rows tiles run while one CTA does a snapshot's columns).
-static bool fused_supported(const bccb_plan_s* p, int ratio = 1) {
+// The last CTA's column tail must not dominate: one snapshot's column work (K1 x L2 points) is
+// at most one rows CTA's work (TR x L1 points).
+static bool fused_supported(const bccb_plan_s* p) {
   static const int env = [] {
     const char* e = getenv("BCCB_FUSE_COLS");
     return e ? atoi(e) : 1;
@@ -725,7 +723,7 @@ static bool fused_supported(const bccb_plan_s* p, int ratio = 1) {
   if (!env) return false;
   const AxisPrec& a = rows_axis(p->ax1);
   const int tr = zs_threads(p->ax1) / a.R;
-  if ((long long)p->ax1.K * p->L2 > (long long)ratio * tr * p->L1) return false;
+  if ((long long)p->ax1.K * p->L2 > (long long)tr * p->L1) return false;
   const AxisPrec& c = p->ax2.s;
   const int trc = std::min(zs_threads(p->ax1) / c.R, p->ax1.K);
   if (trc < 1 || p->ax1.K % trc != 0) return false;
@@ -1318,90 +1316,6 @@ static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const E
   return fail(BCCB_ERR_UNSUPPORTED, "no small-grid specialisation");
 }
 
-// ---- persistent dataflow solver (fused-column shapes, e.g. config 2)
-// Opt-in (BCCB_PERSIST=1): at config 2 the per-snapshot chain (rows tiles -> one CTA's column
-// pass -> next step's tiles) is longer than the time the queue takes to cycle through the
-// batch, so CTAs wait; measured 130 vs 153 G gpi/s for the two-stream per-pass schedule.
-static bool persist_supported() {
-  static const int env = [] {
-    const char* e = getenv("BCCB_PERSIST");
-    return e ? atoi(e) : 0;
-  }();
-  return env != 0;
-}
-
-#define PERSIST_SHAPES(X)  \
-  X(16, 16, 2, 16, 3)      /* config 2, KP 16 engine */ \
-  X(32, 8, 1, 16, 2)       /* config 2, KP 32 engine */
-
-template <typename KernelT>
-static int launch_persistent_kernel(KernelT k, const LaunchShape& sh, int total, const PersistArgs& A,
-                                    cudaStream_t st) {
-  int rc = prep_smem(k, sh.smem);
-  if (rc) return rc;
-  int occ = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, sh.threads, sh.smem));
-  if (occ < 1) return fail(BCCB_ERR_UNSUPPORTED, "persistent solver does not fit on an SM");
-  const unsigned grid = (unsigned)std::min<long long>(total, (long long)occ * num_sms());
-  ProfEvent* pe;
-  prof_before(KIND_ROWS, st, &pe);
-  k<<<grid, sh.threads, sh.smem, st>>>(A);
-  prof_after(pe, st);
-  LAUNCH_CHECK();
-  return BCCB_OK;
-}
-
-// Returns BCCB_ERR_UNSUPPORTED (without launching) when the shape has no persistent kernel.
-static int launch_fista_persistent(bccb_plan_s* p, int batch, int first, int iters, const Workspace& w,
-                                   const EpiFista& e, const FusedCols& fc, cudaStream_t st) {
-  const AxisPrec& a = rows_axis(p->ax1);
-  const AxisPrec& c = p->ax2.s;
-  const int key = fast_key(a);
-  bool have = false;
-#define PERSIST_KEY(KP_, R_, MO_, KP2_, MINB_) \
-  if (key == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_) have = true;
-  PERSIST_SHAPES(PERSIST_KEY)
-#undef PERSIST_KEY
-  if (!have) return BCCB_ERR_UNSUPPORTED;
-  const long long total = (long long)(iters + 1) * batch * fc.cps;
-  if (total >= (1LL << 31)) return BCCB_ERR_UNSUPPORTED;
-  int rc = upload_beta(p, first + iters, st);
-  if (rc) return rc;
-  LaunchShape sh;
-  sh.threads = zs_threads(p->ax1);
-  sh.TR = sh.threads / a.R;
-  const int pitch = (a.R % 2 == 1) ? a.R : a.R + 1;
-  const int pitch2 = (c.R % 2 == 1) ? c.R : c.R + 1;
-  const size_t rows_area = (size_t)sh.TR * (p->ax1.K + 2) + (size_t)sh.TR * a.KP * pitch;
-  const size_t cols_area = (size_t)fc.TRc * (p->ax2.K + 1) + (size_t)fc.TRc * c.KP * pitch2;
-  const size_t tw = (size_t)(a.KP + a.Mo) * a.R;
-  PersistArgs A;
-  A.tw_off = (int)std::max(rows_area, cols_area);
-  sh.smem = ((size_t)A.tw_off + (tw * 8 <= 8192 ? tw : 0)) * sizeof(float2);
-  A.G = rows_geo(p, batch, sh, true, true);
-  A.ax = rows_use_kp16(p->ax1) ? p->ax1.dev_s() : p->ax1.dev<float2>();
-  A.io = RowsIO<float2>{(const float2*)w.V, (float2*)w.U};
-  A.epi = e;
-  A.flags = (unsigned*)w.flags;
-  A.fc = fc;
-  A.beta = p->beta_dev;
-  A.done = w.counters + batch;
-  A.queue = w.counters + 2 * batch;
-  A.tiles_per_snap = fc.cps;
-  A.batch = batch;
-  A.first_iteration = first;
-  A.iterations = iters;
-  CUDA_TRY(cudaMemsetAsync(w.counters, 0, (size_t)(2 * batch + 32) * sizeof(int), st));
-  const bool mom = e.momentum != 0;
-#define PERSIST_CASE(KP_, R_, MO_, KP2_, MINB_)                                                              \
-  if (key == KP_ * 100000 + R_ * 10 + MO_ && c.KP == KP2_)                                                  \
-    return mom ? launch_persistent_kernel(fista_persistent_kernel<KP_, R_, MO_, true, KP2_, MINB_>, sh, (int)total, A, st) \
-               : launch_persistent_kernel(fista_persistent_kernel<KP_, R_, MO_, false, KP2_, MINB_>, sh, (int)total, A, st);
-  PERSIST_SHAPES(PERSIST_CASE)
-#undef PERSIST_CASE
-  return BCCB_ERR_UNSUPPORTED;
-}
-
 extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int iterations,
                               double mu, const double* tau,
                               const void* bhat_box, const void* extra, void* c, void* d,
@@ -1451,17 +1365,6 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   // the skipped zeros are written back by one final pass
   const bool zs = fast_supported(p, batch, extra);
   if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes(p, batch), st));
-
-  // Fused-column shapes: one persistent launch runs every step (dataflow over snapshots)
-  if (zs && fused_supported(p, 4) && persist_supported()) {
-    const float2* bh0 = (const float2*)bhat_box;
-    FusedCols fc = make_fused(p, batch, w, (const float2*)w.D, (const float2*)w.P, bh0);
-    EpiFista ep = e;
-    ep.it = first_iteration;
-    rc = launch_fista_persistent(p, batch, first_iteration, iterations, w, ep, fc, st);
-    if (rc == BCCB_OK) return launch_zero_segments(p, batch, w, e.c, e.d, st);
-    if (rc != BCCB_ERR_UNSUPPORTED) return rc;
-  }
 
   // Sub-batch split: two halves of the batch run on two streams, so one half's (latency-bound)
   // column pass and kernel tails overlap the other half's rows pass.  Snapshots are

@@ -486,16 +486,6 @@ struct FusedCols {
   int K1;
 };
 
-// acquire / release on a per-snapshot progress word (persistent solver)
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
 // Shared-memory twiddle staging of the specialised rows pass: tables of at most 8 KB are
 // staged (short-latency LDS instead of L1 round trips, measured +1% at config 2); larger ones
 // are read through L1 (a 36 KB table at L1 = 4096 would cost a resident CTA per SM, measured
@@ -666,15 +656,13 @@ struct AdmmSplitPolicy {
 
 // One tile (TR lines of one snapshot) of the specialised rows pass, complex64 band engine,
 // state policy Pol.  `tile` indexes the tile (and its flag words); with KP2 > 0 and do_fwd,
-// the last tile of a snapshot to arrive runs that snapshot's column pass and, in the
-// persistent solver (done != null), publishes `done[b] = step + 1`.  Streaming state / band
-// loads bypass L1 (ld.global.cg): in the persistent solver another SM wrote them in an
-// earlier step.
+// the last tile of a snapshot to arrive runs that snapshot's column pass.  Streaming state /
+// band loads bypass L1 (ld.global.cg): they are read once.
 template <int KP, int R, int MO, typename Pol, bool ZS, int KP2>
 __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
                                           const typename Pol::Args& epi, unsigned* __restrict__ flags,
                                           const FusedCols& fc, int tile, const float2* tw1s, const float2* tw2s,
-                                          float2* Xs, int* done, int step) {
+                                          float2* Xs) {
   using TS = TileShape<KP, R, MO>;
   using St = typename Pol::S;
   constexpr int NT = TS::NT, TR = TS::TR, K = TS::K, XP = TS::XP, PITCH = TS::PITCH, SP = TS::SP;
@@ -874,13 +862,6 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       __threadfence();                     // acquire the other CTAs' U tiles
       for (int l0 = 0; l0 < fc.K1; l0 += fc.TRc)
         cols_block<KP2>(fc.G, fc.ax, fc.io, (long long)b * fc.K1 + l0, fc.TRc, Xs);
-      if (done) {
-        __syncthreads();                   // every thread's V stores precede the release
-        if (tid == 0) {
-          __threadfence();
-          st_release_gpu(done + b, step + 1);
-        }
-      }
     }
   }
 }
@@ -895,65 +876,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
-  rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs, nullptr, 0);
-}
-
-// Persistent dataflow solver for the fused-column shapes (config 2): one launch runs all
-// T + 1 steps.  Work items (step j, snapshot b, tile) are handed out in order by an atomic
-// queue; a step-j tile of snapshot b waits (acquire) until the column pass of step j - 1 of b
-// has published done[b] >= j.  Every item a CTA waits on was taken earlier by a running CTA,
-// so the wait chain always ends at an item with nothing to wait for (no co-residency
-// assumption).  Snapshots at different steps overlap, so there are no per-step kernel
-// boundaries, drains or wave tails; the twiddles are staged in shared memory once.
-struct PersistArgs {
-  Geo G;
-  AxisT<float2> ax;
-  RowsIO<float2> io;
-  EpiFista epi;
-  unsigned* flags;
-  FusedCols fc;
-  const double* beta;    // [t_end + 1]
-  int* queue;            // work-item counter (zeroed before the launch)
-  int* done;             // [B] column passes completed (zeroed before the launch)
-  int tiles_per_snap, batch, first_iteration, iterations;
-  int tw_off;            // float2 offset of the staged twiddles (past the rows and cols tiles)
-};
-
-template <int KP, int R, int MO, bool MOM, int KP2, int MINB>
-__global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB) fista_persistent_kernel(PersistArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* Xs = reinterpret_cast<float2*>(smem_raw);
-  const float2* tw1s;
-  const float2* tw2s;
-  stage_twiddles<KP, R, MO>(A.ax, Xs + A.tw_off, tw1s, tw2s);
-  __shared__ int s_item[2];
-  const int per_step = A.batch * A.tiles_per_snap;
-  const int total = (A.iterations + 1) * per_step;
-  const int tid = threadIdx.x;
-  for (int n = 0;; n ^= 1) {
-    if (tid == 0) s_item[n] = atomicAdd(A.queue, 1);
-    __syncthreads();
-    const int item = s_item[n];
-    if (item >= total) break;
-    const int j = item / per_step, rem = item - j * per_step;
-    const int b = rem / A.tiles_per_snap;
-    const int t = A.first_iteration - 1 + j;
-    Geo G = A.G;
-    G.do_inv = j > 0;
-    G.do_fwd = j < A.iterations;
-    if (G.do_inv) {
-      if (tid == 0) {
-        while (ld_acquire_gpu(A.done + b) < j) __nanosleep(64);
-        __threadfence();
-      }
-      __syncthreads();
-    }
-    EpiFista e = A.epi;
-    e.it = t;
-    e.beta_cur = MOM ? A.beta[G.do_inv ? t : A.first_iteration] : 0.0;
-    e.beta_next = MOM ? A.beta[t + 1] : 0.0;
-    rows_tile<KP, R, MO, FistaPolicy<MOM>, true, KP2>(G, A.ax, A.io, e, A.flags, A.fc, rem, tw1s, tw2s, Xs, A.done, j);
-  }
+  rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs);
 }
 
 // ---------------------------------------------------------------- ADMM, spectral dual split
@@ -970,7 +893,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
   const FusedCols nofc{};
-  rows_tile<KP, R, MO, AdmmSplitPolicy, true, 0>(G, ax, io, epi, flags, nofc, blockIdx.x, tw1s, tw2s, Xs, nullptr, 0);
+  rows_tile<KP, R, MO, AdmmSplitPolicy, true, 0>(G, ax, io, epi, flags, nofc, blockIdx.x, tw1s, tw2s, Xs);
 }
 
 // Band stage of the split ADMM column pass (float64 on the box):
