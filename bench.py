@@ -279,7 +279,11 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json copy test)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     fused_cols = n_k[1] == 0
-    rows_bytes = (B_ALG_ROWS[w.solver] + (B_ALG_COLS if fused_cols else 0)) * B * L
+    # algorithmic bytes of one launch: the per-iteration model x the iterations the launch
+    # covers (T / launches: ~1 for the per-pass kernels, T for the whole-solve small-grid and
+    # cluster kernels)
+    iters_per_launch = T / max(n_k[0], 1)
+    rows_bytes = (B_ALG_ROWS[w.solver] + (B_ALG_COLS if fused_cols else 0)) * B * L * iters_per_launch
     achieved = rows_bytes / (rows_ms / 1e3) / 1e9
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -297,7 +301,7 @@ def main():
         "peak_source": peak_src,
         "algorithmic_bytes_per_launch": rows_bytes,
         "bytes_model": (f"{B_ALG_ROWS[w.solver]}{' + 16 (fused K3)' if fused_cols else ''} B/gpi x {B}x{L} gpi "
-                        "per launch (SURVEY 8(d) K4+K2 share)"),
+                        f"x {iters_per_launch:.4g} iterations per launch (SURVEY 8(d) K4+K2 share)"),
         "avg_launch_ms": rows_ms, "share_of_step": ms_k[0] / step_kernel_ms,
         "launch_timing": "profiled extra step, single stream, CUDA events on the launch stream",
         "cols_kernel": ({"avg_launch_ms": cols_ms, "achieved": B_ALG_COLS * B * L / (cols_ms / 1e3) / 1e9,
