@@ -144,9 +144,10 @@ struct AxisPrec {
 
 struct AxisHost {
   int N = 0, K = 0;
-  // complex64 engine (KP <= 32), complex128 engine (KP <= 16), complex64 column-pass engine
-  // (KP <= 16: more threads for the few, short column lines)
-  AxisPrec f, d, s;
+  // complex64 engine (KP <= 32), complex128 engine (KP <= 16), complex64 streaming engine
+  // (KP <= 16: the KP16 rows engine and the column pass) and its KP <= 8 variant (column
+  // passes with few lines: twice the threads per line, shorter latency chains)
+  AxisPrec f, d, s, s8;
   template <typename C>
   const AxisPrec& prec() const;
   template <typename C>
@@ -163,16 +164,17 @@ struct AxisHost {
     a.tw2 = (const C*)p.tw2;
     return a;
   }
-  AxisT<float2> dev_s() const {
+  AxisT<float2> dev_s(bool narrow = false) const {
+    const AxisPrec& q = narrow ? s8 : s;
     AxisT<float2> a;
     a.N = N;
     a.K = K;
-    a.KP = s.KP;
-    a.R = s.R;
-    a.Mo = s.Mo;
-    a.pitch = s.pitch;
-    a.tw1 = (const float2*)s.tw1;
-    a.tw2 = (const float2*)s.tw2;
+    a.KP = q.KP;
+    a.R = q.R;
+    a.Mo = q.Mo;
+    a.pitch = q.pitch;
+    a.tw1 = (const float2*)q.tw1;
+    a.tw2 = (const float2*)q.tw2;
     return a;
   }
 };
@@ -229,7 +231,7 @@ static int upload_twiddles(int N, AxisPrec& ap) {
 
 // Choose the register DFT size KP (largest power of two dividing N, <= 32 and <= the band),
 // round the band up to a multiple of KP and build both precisions' twiddle tables.
-static int make_axis(int N, int Kreq, AxisHost& ax) {
+static int make_axis(int N, int Kreq, AxisHost& ax, bool cols) {
   int KP = 1;
   while (KP < KP_MAX && N % (KP * 2) == 0) KP *= 2;
   KP = std::min(KP, pow2_ceil(std::max(1, Kreq)));
@@ -238,15 +240,16 @@ static int make_axis(int N, int Kreq, AxisHost& ax) {
   if (K % KP != 0) K = N;  // N is a multiple of KP
   ax.N = N;
   ax.K = K;
-  // column-pass register DFT size (BCCB_COLS_KP overrides for tuning; default 16)
+  // streaming-axis register DFT size: 16 (the KP16 rows engine and the column pass);
+  // BCCB_COLS_KP overrides it for the column axis (tuning)
   static const int cols_kp = [] {
     const char* e = getenv("BCCB_COLS_KP");
     const int v = e ? atoi(e) : 16;
     return (v == 4 || v == 8 || v == 16 || v == 32) ? v : 16;
   }();
-  const int kps[3] = {KP, std::min(KP, KP_MAX_D), std::min(KP, cols_kp)};
-  AxisPrec* aps[3] = {&ax.f, &ax.d, &ax.s};
-  for (int q = 0; q < 3; ++q) {
+  const int kps[4] = {KP, std::min(KP, KP_MAX_D), std::min(KP, cols ? cols_kp : 16), std::min(KP, 8)};
+  AxisPrec* aps[4] = {&ax.f, &ax.d, &ax.s, &ax.s8};
+  for (int q = 0; q < 4; ++q) {
     AxisPrec& ap = *aps[q];
     ap.KP = kps[q];
     ap.R = N / ap.KP;
@@ -261,11 +264,12 @@ static int make_axis(int N, int Kreq, AxisHost& ax) {
   int rc = upload_twiddles<float2>(N, ax.f);
   if (!rc) rc = upload_twiddles<double2>(N, ax.d);
   if (!rc) rc = upload_twiddles<float2>(N, ax.s);
+  if (!rc) rc = upload_twiddles<float2>(N, ax.s8);
   return rc;
 }
 
 static void free_axis(AxisHost& a) {
-  for (AxisPrec* p : {&a.f, &a.d, &a.s}) {
+  for (AxisPrec* p : {&a.f, &a.d, &a.s, &a.s8}) {
     cudaFree(p->tw1);
     cudaFree(p->tw2);
   }
@@ -307,8 +311,8 @@ struct DeviceGuard {
 static int finish_plan(bccb_plan_s* p, int k1req, int k2req) {
   int rc = ensure_device_constants(p->device);
   if (rc) return rc;
-  if ((rc = make_axis(p->L1, k1req, p->ax1))) return rc;
-  if ((rc = make_axis(p->L2, k2req, p->ax2))) return rc;
+  if ((rc = make_axis(p->L1, k1req, p->ax1, false))) return rc;
+  if ((rc = make_axis(p->L2, k2req, p->ax2, true))) return rc;
   return BCCB_OK;
 }
 
@@ -940,12 +944,21 @@ static int launch_rows_admm(const bccb_plan_s* p, int batch, bool inv, bool fwd,
   return BCCB_OK;
 }
 
+// Complex64 column passes run the streaming axis (KP <= 16), or its KP <= 8 variant when the
+// launch has so few threads that latency dominates (config 2: 1024 lines x 16 threads;
+// measured 153 -> 160 G gpi/s; the larger configs lose with KP 8).
+static bool cols_narrow(const bccb_plan_s* p, int batch) {
+  const long long threads = (long long)batch * p->ax1.K * p->ax2.s.R;
+  return p->ax2.s8.KP < p->ax2.s.KP && threads < 65536;
+}
+
 template <typename C>
 static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, const Workspace& w,
                        const C* D, const C* P, const float2* Bh, C* box_out, cudaStream_t st) {
-  // complex64 columns run the streaming (KP <= 8) axis: many more threads for few lines
   const bool stream_axis = std::is_same<C, float2>::value;
-  const LaunchShape sh = stream_axis ? shape_for_prec(p->ax2, p->ax2.s, sizeof(C), (long long)batch * p->ax1.K)
+  const bool narrow = stream_axis && cols_narrow(p, batch);
+  const LaunchShape sh = stream_axis ? shape_for_prec(p->ax2, narrow ? p->ax2.s8 : p->ax2.s, sizeof(C),
+                                                      (long long)batch * p->ax1.K)
                                      : shape_for<C>(p->ax2, (long long)batch * p->ax1.K);
   Geo G;
   G.L1 = p->L1;
@@ -964,7 +977,7 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   io.K1 = p->ax1.K;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   if constexpr (std::is_same<C, float2>::value) {
-    const AxisT<C> ax = p->ax2.dev_s();
+    const AxisT<C> ax = p->ax2.dev_s(narrow);
     KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
   } else {
     const AxisT<C> ax = p->ax2.dev<C>();
@@ -1488,14 +1501,16 @@ static Geo cols_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool
 
 static int launch_cols_admm_split(const bccb_plan_s* p, int batch, const Workspace& w, const AdmmSplitBand& op,
                                   cudaStream_t st) {
-  const LaunchShape sh = shape_for_prec(p->ax2, p->ax2.s, sizeof(float2), (long long)batch * p->ax1.K);
+  const bool narrow = cols_narrow(p, batch);
+  const LaunchShape sh = shape_for_prec(p->ax2, narrow ? p->ax2.s8 : p->ax2.s, sizeof(float2),
+                                        (long long)batch * p->ax1.K);
   const Geo G = cols_geo(p, batch, sh, true, true);
   ColsIO<float2> io{};
   io.U = (const float2*)w.U;
   io.V = (float2*)w.V;
   io.K1 = p->ax1.K;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
-  const AxisT<float2> ax = p->ax2.dev_s();
+  const AxisT<float2> ax = p->ax2.dev_s(narrow);
   KP_DISPATCH_F(ax.KP, return launch_pass<float2>(cols_admm_split_kernel<KPC>, KIND_COLS, grid, sh, st, G, ax, io, op));
   return BCCB_OK;
 }
