@@ -97,6 +97,42 @@ def cpu_iters_for(cfg: int, workers: int, budget_cpu_s: float = 15.0) -> int:
     return max(2, min(t, scenes.workload(cfg).iterations))
 
 
+DENSE_BUDGET = 8 << 30   # the reference's dictionary / DenseGram budget (dictionary.py:17, 163-166)
+
+
+def dense_sample(cfg: int, budget_s: float = 10.0):
+    """The reference's dense O((L1L2)^2) "regular" ISTA (oracle.ista_dense, pinned bitwise to
+    the reference by tests/golden/dense.npz) on snapshot 0, where the DenseGram fits the
+    reference's memory budget (config 1 only).  The Gram build is untimed precompute, as in
+    the reference (SolverResult.total_seconds times the loop only, solvers.py:271-278).
+    OpenBLAS runs with its default threads (the reference's `@`)."""
+    import numpy as np
+    from oracle import bccb_oracle as orc
+    from paper_2509_13592_b200 import scenes
+    w = scenes.workload(cfg)
+    need = w.grid_points ** 2 * 16
+    if need > DENSE_BUDGET:
+        return {"value": None, "unavailable": f"DenseGram needs {need / 2**30:.0f} GiB > the reference's 8 GiB "
+                                              f"budget (MemoryBudgetError, dictionary.py:163-166)"}
+    geom, ys, _ = scenes.make_scene(w, [0])
+    m1, m2 = geom.occupied_coordinates()
+    g = orc.dense_gram(m1, m2, w.l1, w.l2)
+    b = orc.adjoint_fft(m1, m2, w.l1, w.l2, ys[0])
+    tau = w.tau_fraction * float(np.max(np.abs(b)))
+    mu = 1.0 / w.grid_points
+    orc.ista_dense(g, b, tau, mu, 2)                    # warm-up
+    t0 = time.perf_counter()
+    iters = 0
+    while time.perf_counter() - t0 < budget_s and iters < w.iterations:
+        orc.ista_dense(g, b, tau, mu, 5)
+        iters += 5
+    dt = time.perf_counter() - t0
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or str(len(os.sched_getaffinity(0)))
+    return {"value": w.grid_points * iters / dt, "unit": UNIT, "cores": int(threads), "kind": "port",
+            "ms_per_iteration": dt * 1e3 / iters,
+            "sample": f"dense regular-backend ISTA (DenseGram @ c, complex128) on 1 snapshot x {iters} iterations"}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -269,7 +305,7 @@ def main():
     ms_k = (ctypes.c_double * 3)()
     n_k = (ctypes.c_longlong * 3)()
     _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
-    _lib.check(_lib.lib.bccb_set_substreams(int(os.environ.get("BCCB_SUBSTREAMS", "2"))))
+    _lib.check(_lib.lib.bccb_set_substreams(0))        # back to the library default
     rows_ms = ms_k[0] / max(n_k[0], 1)
     cols_ms = ms_k[1] / max(n_k[1], 1)
     step_kernel_ms = ms_k[0] + ms_k[1] + ms_k[2]
@@ -367,8 +403,9 @@ def main():
         finally:
             pool.close()
         cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": f"oracle FISTA (numpy pocketfft, float64) on {workers} snapshots x {iters} iterations, "
-                         f"one process per core; {wall:.1f} s wall"}
+               "sample": f"oracle {w.solver.upper()} (numpy pocketfft, float64) on {workers} snapshots x {iters} "
+                         f"iterations, one process per core; {wall:.1f} s wall",
+               "dense": dense_sample(w.cfg)}
 
     if rank == 0:
         line = {

@@ -169,9 +169,9 @@ long long bccb_launch_count(void);
 int bccb_profile_begin(void);
 int bccb_profile_end(double* ms_by_kind, long long* launches_by_kind);
 
-/* Number of streams a large batch is split over (1..4; default 2, env BCCB_SUBSTREAMS; fewer
- * when a part would have < 2048 lines).  The parts are independent snapshots, so results are
- * bitwise identical either way. */
+/* Number of streams a large batch is split over (1..8; 0 restores the default: env
+ * BCCB_SUBSTREAMS, else 3; fewer when a part would have < 2048 lines).  The parts are
+ * independent snapshots, so results are bitwise identical either way. */
 int bccb_set_substreams(int n);
 
 /* Kernel path: 0 = automatic (small-grid persistent solver, shape-specialised and fused

@@ -82,6 +82,21 @@ def adjoint_dense(m1, m2, l1: int, l2: int, y: np.ndarray) -> np.ndarray:
     return mat.conj().T @ y
 
 
+def dictionary_matrix(m1, m2, l1: int, l2: int) -> np.ndarray:
+    """Explicit M x L1L2 dictionary, row (m1, m2), column l1 + l2*L1 — dictionary.py:83-97."""
+    f1 = -0.5 + np.arange(l1) / l1
+    f2 = -0.5 + np.arange(l2) / l2
+    r1 = np.exp(-2j * np.pi * np.outer(m1, f1))
+    r2 = np.exp(-2j * np.pi * np.outer(m2, f2))
+    return (r2[:, :, None] * r1[:, None, :]).reshape(len(m1), l1 * l2)
+
+
+def dense_gram(m1, m2, l1: int, l2: int) -> np.ndarray:
+    """D_s^H D_s (the regular backend's DenseGram) — dictionary.py:155-168."""
+    mat = dictionary_matrix(m1, m2, l1, l2)
+    return mat.conj().T @ mat
+
+
 def adjoint_fft(m1, m2, l1: int, l2: int, y: np.ndarray) -> np.ndarray:
     """Same b via L1*L2*ifft2 of the signed scatter E[m2, m1] = (-1)^(m1+m2) y_m
     (SURVEY finding 4; matches adjoint_dense to ~1e-15, tests/test_oracle_golden.py)."""
@@ -119,6 +134,17 @@ def ista(eig_t, b, tau: float, mu: float, iterations: int, c0=None) -> np.ndarra
     c = np.zeros(b.size, dtype=np.complex128) if c0 is None else np.array(c0, dtype=np.complex128)
     for it in range(iterations):
         c = prox_step(c, matvec(eig_t, c), b, mu, kappa)
+        _finite(c, it)
+    return c
+
+
+def ista_dense(gram: np.ndarray, b, tau: float, mu: float, iterations: int, c0=None) -> np.ndarray:
+    """ista_solve on the regular backend: G c as a dense O(L^2) product (solvers.py:73-77,
+    264-278) — the reference's dense baseline path."""
+    kappa = mu * tau
+    c = np.zeros(b.size, dtype=np.complex128) if c0 is None else np.array(c0, dtype=np.complex128)
+    for it in range(iterations):
+        c = prox_step(c, gram @ c, b, mu, kappa)
         _finite(c, it)
     return c
 

@@ -113,6 +113,18 @@ extern "C" int bccb_profile_end(double* ms_by_kind, long long* launches_by_kind)
 }
 extern "C" const char* bccb_version(void) { return "bccb_b200 0.1.0 (sm_100a)"; }
 
+// ------------------------------------------------------------------ launch mode
+// Programmatic dependent launch of the pass kernels (BCCB_PDL): 0 off, 1 on with each CTA
+// releasing its dependents right after its griddepcontrol.wait, 2 on with the implicit
+// release at grid completion.
+static int pdl_mode() {
+  static const int m = [] {
+    const char* e = getenv("BCCB_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return m;
+}
+
 // ------------------------------------------------------------------ device init
 static std::mutex g_init_mu;
 static bool g_roots_ready[64];
@@ -130,6 +142,8 @@ static int ensure_device_constants(int device) {
   }
   CUDA_TRY(cudaMemcpyToSymbol(c_roots64, roots, sizeof(roots)));
   CUDA_TRY(cudaMemcpyToSymbol(c_roots64d, rootsd, sizeof(rootsd)));
+  const int trig = pdl_mode() == 1 ? 1 : 0;
+  CUDA_TRY(cudaMemcpyToSymbol(c_pdl_trigger, &trig, sizeof(trig)));
   g_roots_ready[device] = true;
   return BCCB_OK;
 }
@@ -191,7 +205,7 @@ struct bccb_plan_s {
   int M = 0;                       // occupied elements (Gram plans)
   int* occ_dev = nullptr;          // [3][M]: m1, m2 (reduced mod L1 / L2), (m1 + m2) & 1
   int occ_alias = 0;               // some occupied cells alias (M1 > L1 or M2 > L2)
-  static constexpr int MAX_SUB = 4;
+  static constexpr int MAX_SUB = 8;
   cudaStream_t aux[MAX_SUB - 1] = {};   // extra streams of the sub-batch split (created lazily)
   double* beta_dev = nullptr;      // momentum table of the small-grid persistent solver
   size_t beta_cap = 0;
@@ -613,7 +627,22 @@ static int launch_pass(KernelT k, int kind, unsigned grid, const LaunchShape& sh
   if (rc) return rc;
   ProfEvent* pe;
   prof_before(kind, st, &pe);
-  k<<<grid, sh.threads, sh.smem, st>>>(args...);
+  if (pdl_mode() > 0) {
+    // programmatic dependent launch: every kernel of bccb_kernels.cuh starts with pdl_wait()
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(sh.threads);
+    cfg.dynamicSmemBytes = sh.smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k, args...));
+  } else {
+    k<<<grid, sh.threads, sh.smem, st>>>(args...);
+  }
   prof_after(pe, st);
   LAUNCH_CHECK();
   return BCCB_OK;
@@ -1183,8 +1212,8 @@ static int check_singular_admm(const bccb_plan_s* p, double rho) {
 static std::atomic<int> g_substreams{-1};
 
 extern "C" int bccb_set_substreams(int n) {
-  if (n < 1 || n > bccb_plan_s::MAX_SUB) return fail(BCCB_ERR_INVALID, "substreams must be in [1, %d]", bccb_plan_s::MAX_SUB);
-  g_substreams.store(n);
+  if (n < 0 || n > bccb_plan_s::MAX_SUB) return fail(BCCB_ERR_INVALID, "substreams must be in [0, %d]", bccb_plan_s::MAX_SUB);
+  g_substreams.store(n == 0 ? -1 : n);
   return BCCB_OK;
 }
 
@@ -1192,7 +1221,7 @@ static int sub_batches(const bccb_plan_s* p, int batch) {
   int n = g_substreams.load();
   if (n < 0) {
     const char* e = getenv("BCCB_SUBSTREAMS");
-    n = e ? atoi(e) : 2;
+    n = e ? atoi(e) : 3;   // measured best at config 2 with PDL (2: 171, 3: 186, 4: 177 G gpi/s)
   }
   n = std::max(1, std::min(n, bccb_plan_s::MAX_SUB));
   while (n > 1 && (batch < n || (long long)(batch / n) * p->L2 < 2048)) --n;

@@ -20,6 +20,18 @@
 
 namespace bccb {
 
+// Programmatic dependent launch (PDL).  The per-pass kernels are launched with the
+// programmatic-stream-serialization attribute (bccb_capi.cu launch_pass), so the next pass's
+// CTAs are scheduled while this pass drains.  griddepcontrol.wait blocks until the previous
+// grid on the stream has completed and its writes are visible (a no-op without the
+// attribute); nothing before it may touch memory another pass writes.  With c_pdl_trigger
+// set, each CTA then releases its dependents at once.
+__constant__ int c_pdl_trigger;
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (c_pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 struct Geo {
   int L1, L2;
   long long rows;  // total lines in this launch
@@ -303,6 +315,7 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
 
 template <int KP, typename C>
 __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cols_block<KP>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR, reinterpret_cast<C*>(smem_raw));
 }
@@ -311,6 +324,7 @@ __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT
 // Generic pass A for plain-vector epilogues.
 template <int KP, typename C, typename E = EpiVector<C>>
 __global__ void __launch_bounds__(256) rows_vector_kernel(Geo G, AxisT<C> ax, RowsIO<C> io, E epi) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int R = ax.R, K = ax.K;
@@ -355,6 +369,7 @@ __global__ void __launch_bounds__(256, MINB) rows_fista_kernel(Geo G, AxisT<floa
                                                                EpiFista epi) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* smem = reinterpret_cast<float2*>(smem_raw);
+  pdl_wait();
   const int R = ax.R, K = ax.K;
   const int ii = threadIdx.x / R, s = threadIdx.x - ii * R;
   const long long row0 = (long long)blockIdx.x * G.TR;
@@ -876,6 +891,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
+  pdl_wait();
   rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs);
 }
 
@@ -892,6 +908,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
+  pdl_wait();
   const FusedCols nofc{};
   rows_tile<KP, R, MO, AdmmSplitPolicy, true, 0>(G, ax, io, epi, flags, nofc, blockIdx.x, tw1s, tw2s, Xs);
 }
@@ -929,6 +946,7 @@ struct AdmmSplitBand {
 template <int KP>
 __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_admm_split_kernel(Geo G, AxisT<float2> ax,
                                                                              ColsIO<float2> io, AdmmSplitBand op) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cols_block<KP, float2, true, AdmmSplitBand>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR,
                                                reinterpret_cast<float2*>(smem_raw), op);
@@ -945,6 +963,7 @@ struct BoxIn {
 template <int KP, typename C>
 __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_box_kernel(Geo G, AxisT<C> ax, ColsIO<C> io,
                                                                       BoxIn<C> op) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cols_block<KP, C, true, BoxIn<C>>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR, reinterpret_cast<C*>(smem_raw),
                                     op);
@@ -991,6 +1010,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int KP, int R, int MO, bool ZS>
 __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
     rows_admm_fast_kernel(Geo G, AxisT<double2> ax, RowsIO<double2> io, EpiAdmm epi, unsigned* __restrict__ flags) {
+  pdl_wait();
   constexpr int NT = R > 256 ? R : 256;
   constexpr int TR = NT / R;
   constexpr int K = KP * MO;
@@ -1133,6 +1153,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
 template <int KP, int R>
 __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_z_kernel(Geo G, double2* z,
                                                                             const unsigned* __restrict__ flags) {
+  pdl_wait();
   constexpr int NT = R > 256 ? R : 256;
   constexpr int TR = NT / R;
   const int tid = threadIdx.x;
@@ -1164,6 +1185,7 @@ struct SmallArgs {
 
 template <int KP1, int KP2, bool MOM>
 __global__ void __launch_bounds__(1024, 1) small_fista_kernel(SmallArgs A) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L1 = A.L1, L2 = A.L2, L = L1 * L2, K1 = A.K1;
   const int b = blockIdx.x;
@@ -1296,6 +1318,7 @@ struct ClusterArgs {
 
 template <bool MOM>
 __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 1) cluster64_fista_kernel(ClusterArgs A) {
+  pdl_wait();
   namespace cgp = cooperative_groups;
   constexpr int L = 64, CL = 8, RPC = L / CL;
   cgp::cluster_group cluster = cgp::this_cluster();
@@ -1435,6 +1458,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 1) cluster64_fi
 template <int KP, int R, typename T2 = float2>
 __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G, double2* c, T2* d,
                                                                           const unsigned* __restrict__ flags) {
+  pdl_wait();
   constexpr int NT = R > 256 ? R : 256;
   constexpr int TR = NT / R;
   const int tid = threadIdx.x;
@@ -1456,6 +1480,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G,
 template <int KP, int CH>
 __global__ void __launch_bounds__(256) rows_admm_kernel(Geo G, AxisT<double2> ax, RowsIO<double2> io,
                                                         EpiAdmm epi) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   const int R = ax.R, K = ax.K;
