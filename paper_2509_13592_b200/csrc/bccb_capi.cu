@@ -1600,26 +1600,78 @@ static int admm_run_split(bccb_plan_s* p, int batch, int first_iteration, int it
   op.rhoL = rho * (double)p->L1 * (double)p->L2;
   op.K1 = p->ax1.K;
   op.K2 = p->ax2.K;
+  // sub-batch split over streams, as in bccb_fista_run (independent snapshots: bitwise equal).
+  // Not with c_last: its complex128 synthesis borrows the whole U region mid-iteration, which a
+  // concurrent part's column pass still reads.
+  const int nsub = c_last ? 1 : sub_batches(p, batch);
+  if (nsub > 1 && (rc = ensure_aux_streams(p, nsub))) return rc;
+  struct Sub {
+    int b0, nb;
+    cudaStream_t st;
+    Workspace w;
+    EpiAdmmSplit e;
+    AdmmSplitBand op;
+    double2 *z, *v, *c_last;
+  } sub[bccb_plan_s::MAX_SUB];
+  for (int q = 0; q < nsub; ++q) {
+    Sub& u = sub[q];
+    u.b0 = (int)((long long)batch * q / nsub);
+    u.nb = (int)((long long)batch * (q + 1) / nsub) - u.b0;
+    u.st = q == 0 ? st : p->aux[q - 1];
+    const long long inter = (long long)u.b0 * p->ax1.K * p->L2;
+    const long long boxo = (long long)u.b0 * p->ax1.K * p->ax2.K;
+    const long long off = (long long)u.b0 * p->L1 * p->L2;
+    u.w = w;
+    u.w.U = (float2*)w.U + inter;
+    u.w.V = (float2*)w.V + inter;
+    u.w.vs = (double2*)w.vs + boxo;
+    u.w.cb = (double2*)w.cb + boxo;
+    u.w.flags = w.flags + zs_flag_bytes(p, u.b0);
+    u.z = z + off;
+    u.v = v + off;
+    u.c_last = c_last ? c_last + off : nullptr;
+    u.e = e;
+    u.e.z = u.z;
+    u.e.r = u.v;
+    u.e.tau = tau + u.b0;
+    u.e.first_bad = first_bad + u.b0;
+    u.op = op;
+    u.op.Bh = bhat + boxo;
+    u.op.vs = (double2*)u.w.vs;
+  }
+  if (nsub > 1) {
+    CUDA_TRY(cudaEventRecord(p->ev_fork, st));
+    for (int q = 1; q < nsub; ++q) CUDA_TRY(cudaStreamWaitEvent(p->aux[q - 1], p->ev_fork, 0));
+  }
   const int t_end = first_iteration + iterations;
-  if ((rc = launch_rows_admm_split(p, batch, false, true, w, e, st))) return rc;
+  for (int q = 0; q < nsub; ++q)
+    if ((rc = launch_rows_admm_split(p, sub[q].nb, false, true, sub[q].w, sub[q].e, sub[q].st))) return rc;
   for (int t = first_iteration; t < t_end; ++t) {
     const bool last = t + 1 == t_end;
-    op.cb_out = (last && c_last) ? (double2*)w.cb : nullptr;
-    if ((rc = launch_cols_admm_split(p, batch, w, op, st))) return rc;
-    if (last && c_last) {
-      // c = a (z - r) + IFFT2u(Cb) from the state before the last update; the complex128
-      // synthesis runs through U (free: the last rows pass has no forward half)
-      if ((rc = launch_zero_segments(p, batch, w, z, v, st))) return rc;
-      Workspace wu = w;
-      wu.V = w.U;
-      if ((rc = launch_cols_box_z(p, batch, wu, (const double2*)w.cb, st))) return rc;
-      const EpiCombine ec{z, v, c_last, a};
-      if ((rc = launch_rows_combine_z(p, batch, wu, ec, st))) return rc;
+    for (int q = 0; q < nsub; ++q) {
+      Sub& u = sub[q];
+      u.op.cb_out = (last && c_last) ? (double2*)u.w.cb : nullptr;
+      if ((rc = launch_cols_admm_split(p, u.nb, u.w, u.op, u.st))) return rc;
+      if (last && c_last) {
+        // c = a (z - r) + IFFT2u(Cb) from the state before the last update; the complex128
+        // synthesis runs through U (free: the last rows pass has no forward half)
+        if ((rc = launch_zero_segments(p, u.nb, u.w, u.z, u.v, u.st))) return rc;
+        Workspace wu = u.w;
+        wu.V = u.w.U;
+        if ((rc = launch_cols_box_z(p, u.nb, wu, (const double2*)u.w.cb, u.st))) return rc;
+        const EpiCombine ec{u.z, u.v, u.c_last, a};
+        if ((rc = launch_rows_combine_z(p, u.nb, wu, ec, u.st))) return rc;
+      }
+      u.e.it = t;
+      if ((rc = launch_rows_admm_split(p, u.nb, true, !last, u.w, u.e, u.st))) return rc;
     }
-    e.it = t;
-    if ((rc = launch_rows_admm_split(p, batch, true, !last, w, e, st))) return rc;
   }
-  if ((rc = launch_zero_segments(p, batch, w, z, v, st))) return rc;
+  for (int q = 0; q < nsub; ++q)
+    if ((rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].z, sub[q].v, sub[q].st))) return rc;
+  for (int q = 1; q < nsub; ++q) {
+    CUDA_TRY(cudaEventRecord(p->ev_join[q - 1], p->aux[q - 1]));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join[q - 1], 0));
+  }
   // v = r + IFFT2u(vs)
   if ((rc = launch_cols_box_z(p, batch, w, (const double2*)w.vs, st))) return rc;
   const EpiCombine ev{v, nullptr, v, 1.0};
