@@ -80,15 +80,20 @@ def _circ(a: float, b: float) -> float:
     return min(d, 1.0 - d)
 
 
+def draw_targets(rng: np.random.Generator, k_range: tuple[int, int]) -> list[Target]:
+    """Unit-modulus random-phase targets, harmonics uniform on [-1/2, 1/2)^2, count drawn from
+    [k_range[0], k_range[1]] — the reference's draw sequence (experiments.py:185-194)."""
+    count = int(rng.integers(k_range[0], k_range[1] + 1))
+    f1 = rng.uniform(-0.5, 0.5, count)
+    f2 = rng.uniform(-0.5, 0.5, count)
+    phase = rng.uniform(0.0, 2.0 * np.pi, count)
+    return [Target(float(f1[i]), float(f2[i]), complex(np.exp(1j * phase[i]))) for i in range(count)]
+
+
 def draw_scene_targets(w: Workload, rng: np.random.Generator) -> list[Target]:
     k = w.targets
     if w.amplitudes == "unit":
-        # identical draw sequence to experiments.draw_targets(rng, (k, k)) (experiments.py:185-194)
-        count = int(rng.integers(k, k + 1))
-        f1 = rng.uniform(-0.5, 0.5, count)
-        f2 = rng.uniform(-0.5, 0.5, count)
-        phase = rng.uniform(0.0, 2.0 * np.pi, count)
-        return [Target(float(f1[i]), float(f2[i]), complex(np.exp(1j * phase[i]))) for i in range(count)]
+        return draw_targets(rng, (k, k))
     if w.separated:
         # rejection sampling: every pair separated by >= 1/L1 in f1 OR >= 1/L2 in f2 (circular)
         f1s: list[float] = []
