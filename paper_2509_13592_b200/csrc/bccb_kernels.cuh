@@ -247,13 +247,45 @@ struct ColsIO {
 // Default band stage of the column pass: Y = D*X + P*Bh from ColsIO.
 struct BandMulAdd {};
 
+// Band operands of a thread's first output (idx = threadIdx.x) of the default band stage,
+// D[k1][o] and P*Bh: they do not depend on the previous pass, so cols_kernel fetches them
+// before its grid-dependency wait.
+template <typename C>
+struct ColsPre {
+  C d, pb;
+  bool ok;
+};
+
+template <typename C>
+__device__ __forceinline__ ColsPre<C> cols_prefetch(const Geo& G, const AxisT<C>& ax, const ColsIO<C>& io,
+                                                    long long row0, int TR) {
+  ColsPre<C> pre;
+  pre.ok = false;
+  const int K = ax.K;
+  const int idx = threadIdx.x;
+  if (idx >= TR * K) return pre;
+  const int i2 = idx / K, o = idx - i2 * K;
+  const long long g2 = row0 + i2;
+  if (g2 >= G.rows) return pre;
+  const long long k1 = g2 % io.K1;
+  if (io.D) pre.d = __ldg(io.D + k1 * K + o);
+  pre.pb = cmake(decltype(C::x)(0), decltype(C::x)(0));
+  if (io.Bh) {
+    pre.pb = to_c(io.Bh[g2 * K + o], C{});
+    if (io.P) pre.pb = cmul(pre.pb, __ldg(io.P + k1 * K + o));
+  }
+  pre.ok = true;
+  return pre;
+}
+
 // Column lines [row0, row0 + TR) (line = (snapshot b, column k1): length L2, band K2) processed
 // by one CTA of TR * ax.R threads (threads beyond that idle).  Shared by cols_kernel and the
 // fused rows kernel.  smem: TR x (K+1) band tile + TR x KP x pitch transpose buffer.
 // Op (other than BandMulAdd) replaces the band stage: y = op(line, o, X or 0).
 template <int KP, typename C, bool U_GLOBAL = true, typename Op = BandMulAdd>
 __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, const ColsIO<C>& io, long long row0,
-                                           int TR, C* smem, const Op& op = Op{}) {
+                                           int TR, C* smem, const Op& op = Op{},
+                                           const ColsPre<C>& pre = ColsPre<C>{}) {
   const int R = ax.R, K = ax.K, N = ax.N;
   const int XP = K + 1, SP = KP * ax.pitch;
   const int nthr = TR * R;
@@ -281,6 +313,14 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     if (g2 >= G.rows) continue;
     C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
     if constexpr (std::is_same<Op, BandMulAdd>::value) {
+      if (pre.ok && idx == tid) {
+        if (G.do_fwd) {
+          y = band_fwd_output(S + i2 * SP, o, KP, ax);
+          if (io.D) y = cmul(y, pre.d);
+        }
+        Xs[i2 * XP + o] = io.Bh ? cadd(y, pre.pb) : y;
+        continue;
+      }
       const long long k1 = g2 % io.K1;
       if (G.do_fwd) {
         y = band_fwd_output(S + i2 * SP, o, KP, ax);
@@ -315,9 +355,11 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
 
 template <int KP, typename C>
 __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT<C> ax, ColsIO<C> io) {
-  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cols_block<KP>(G, ax, io, (long long)blockIdx.x * G.TR, G.TR, reinterpret_cast<C*>(smem_raw));
+  const long long row0 = (long long)blockIdx.x * G.TR;
+  const ColsPre<C> pre = cols_prefetch(G, ax, io, row0, G.TR);
+  pdl_wait();
+  cols_block<KP>(G, ax, io, row0, G.TR, reinterpret_cast<C*>(smem_raw), BandMulAdd{}, pre);
 }
 
 // ------------------------------------------------------------------ pass A kernels
@@ -708,16 +750,29 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   __shared__ unsigned live_rows[(TR + 31) / 32];   // lines whose next operator input is nonzero
   auto live_rows_zero = [&](int i) { live_rows[i] = 0u; };
 
+  // first state chunk in flight while the band tile loads and the inverse DFT runs.  The
+  // flags and the state were last written by the previous rows pass, which completed before
+  // the column pass between them released this grid (pdl_wait there), so they are read before
+  // this grid's own dependency wait; the band tile V comes from that column pass (after it).
+  // Early only for short lines (config 2: +2.7%); the long-line shapes keep the load order
+  // band tile -> state (configs 4/5 measured 1-2% slower with the state first).
+  constexpr bool EARLY = R <= 16;
+  St sb[CH];
+  if (EARLY && G.do_inv) {
+#pragma unroll
+    for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
+  }
+  pdl_wait();
   if (G.do_inv) {
     // band tile V[b][k][l20 + ii] -> Xs[ii][k]
     for (int idx = tid; idx < TR * K; idx += NT) {
       const int k = idx / TR, i2 = idx % TR;
       Xs[i2 * XP + k] = __ldcg(io.V + vbase + (long long)k * L2 + i2);
     }
-    // first state chunk in flight while the inverse DFT runs
-    St sb[CH];
+    if (!EARLY) {
 #pragma unroll
-    for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
+      for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
+    }
     if (G.do_fwd && tid < (TR + 31) / 32) live_rows_zero(tid);
     __syncthreads();
     unsigned nfl = 0;
@@ -891,7 +946,6 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
-  pdl_wait();
   rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs);
 }
 
@@ -908,7 +962,6 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
-  pdl_wait();
   const FusedCols nofc{};
   rows_tile<KP, R, MO, AdmmSplitPolicy, true, 0>(G, ax, io, epi, flags, nofc, blockIdx.x, tw1s, tw2s, Xs);
 }
