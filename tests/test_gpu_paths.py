@@ -48,7 +48,7 @@ def scene_problem(cfg, nsnap, iters=None):
     return w, geom, op, bs, taus
 
 
-@pytest.mark.parametrize("cfg,nsnap,iters", [(1, 3, 200), (2, 6, 150), (4, 2, 60), (5, 1, 8)])
+@pytest.mark.parametrize("cfg,nsnap,iters", [(1, 3, 200), (2, 6, 150), (3, 2, 80), (4, 2, 60), (5, 1, 8)])
 def test_fista_auto_vs_generic_vs_oracle(cfg, nsnap, iters, generic_path):
     w, geom, op, bs, taus = scene_problem(cfg, nsnap)
     mu = 1.0 / (w.l1 * w.l2)
