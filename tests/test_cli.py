@@ -189,3 +189,19 @@ def test_verify_and_gram_dump(tmp_path, gold, capsys):
     assert "cap" in capsys.readouterr().out
     assert main(["verify", "--config", write_config(tmp_path / "s.json", dict(VERIFY, l1=32)), "--set", "cap=256"]) == 0
     capsys.readouterr()
+
+
+@pytest.mark.gpu
+def test_bench_writes_records(tmp_path, capsys):
+    """pkg/tests/test_cli.py:236-258 (figures aside: the CSVs they are drawn from)."""
+    config = write_config(tmp_path / "bench.json", {"m1_count": 10, "m2_count": 6, "element_count": 24, "l2": 8,
+                                                    "l1_values": [8, 16], "iteration_values": [10], "trials": 1,
+                                                    "base_seed": 7, "solvers": ["ista", "admm"]})
+    out = tmp_path / "bench"
+    assert main(["bench", "--config", config, "--output-dir", str(out)]) == 0
+    for name in ("records.csv", "summary.csv", "plot_data.csv"):
+        assert (out / name).exists(), name
+    assert len((out / "records.csv").read_text().splitlines()) == 1 + 2 * 2 * 1 * 1
+    assert main(["bench", "--config", write_config(tmp_path / "bad.json", {"m1_counts": 10}),
+                 "--output-dir", str(tmp_path)]) == 1
+    assert "m1_counts" in capsys.readouterr().err
