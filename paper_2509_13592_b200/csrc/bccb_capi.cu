@@ -981,6 +981,16 @@ static bool cols_narrow(const bccb_plan_s* p, int batch) {
   return p->ax2.s8.KP < p->ax2.s.KP && threads < 65536;
 }
 
+// Warp-per-line column pass (cols_warp_kernel): lines of 32 threads x KP = 8 with a band of 32
+// (L2 = 256, K2 = 32: config 2).  BCCB_COLS_WARP=0 keeps the shared-memory column pass.
+static bool cols_warp_supported(const bccb_plan_s* p, const AxisPrec& a) {
+  static const int env = [] {
+    const char* e = getenv("BCCB_COLS_WARP");
+    return e ? atoi(e) : 1;
+  }();
+  return env && a.KP == 8 && a.R == 32 && p->ax2.K == 32;
+}
+
 template <typename C>
 static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, const Workspace& w,
                        const C* D, const C* P, const float2* Bh, C* box_out, cudaStream_t st) {
@@ -1007,6 +1017,15 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   if constexpr (std::is_same<C, float2>::value) {
     const AxisT<C> ax = p->ax2.dev_s(narrow);
+    if (cols_warp_supported(p, narrow ? p->ax2.s8 : p->ax2.s)) {
+      // one warp per column line, 8 lines per CTA
+      LaunchShape shw;
+      shw.TR = 8;
+      shw.threads = 256;
+      shw.smem = 0;
+      const unsigned gw = (unsigned)((G.rows + 7) / 8);
+      return launch_pass<C>(cols_warp_kernel<8>, KIND_COLS, gw, shw, st, G, ax, io);
+    }
     KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
   } else {
     const AxisT<C> ax = p->ax2.dev<C>();
