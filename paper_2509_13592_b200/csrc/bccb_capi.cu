@@ -981,14 +981,32 @@ static bool cols_narrow(const bccb_plan_s* p, int batch) {
   return p->ax2.s8.KP < p->ax2.s.KP && threads < 65536;
 }
 
-// Warp-per-line column pass (cols_warp_kernel): lines of 32 threads x KP = 8 with a band of 32
-// (L2 = 256, K2 = 32: config 2).  BCCB_COLS_WARP=0 keeps the shared-memory column pass.
+// Warp-per-line column pass (cols_warp_kernel): lines of R = 32 threads with a band of 32
+// (KP = 8 or 16): config 2's L2 = 256 (193 -> 205 G gpi/s), config 4's L2 = 512 (288 -> 297 G).
+// A band of 64 (config 3's split ADMM, NSET = 2) measured neutral (299 vs 298 G) and keeps the
+// shared-memory pass.  BCCB_COLS_WARP=0 keeps the shared-memory column pass everywhere.
 static bool cols_warp_supported(const bccb_plan_s* p, const AxisPrec& a) {
   static const int env = [] {
     const char* e = getenv("BCCB_COLS_WARP");
     return e ? atoi(e) : 1;
   }();
-  return env && a.KP == 8 && a.R == 32 && p->ax2.K == 32;
+  if (!env || a.R != 32) return false;
+  const int K = p->ax2.K;
+  return K == 32 && (a.KP == 8 || a.KP == 16);
+}
+
+template <typename Op, typename... Args>
+static int launch_cols_warp(const bccb_plan_s* p, const AxisPrec& a, const Geo& G, cudaStream_t st,
+                            Args... args) {
+  LaunchShape shw;
+  shw.TR = 8;
+  shw.threads = 256;
+  shw.smem = 0;
+  const unsigned gw = (unsigned)((G.rows + 7) / 8);
+  const int K = p->ax2.K;
+  if (K == 32 && a.KP == 8) return launch_pass<float2>(cols_warp_kernel<8, 1, Op>, KIND_COLS, gw, shw, st, G, args...);
+  if (K == 32 && a.KP == 16) return launch_pass<float2>(cols_warp_kernel<16, 1, Op>, KIND_COLS, gw, shw, st, G, args...);
+  return fail(BCCB_ERR_UNSUPPORTED, "no warp column pass for this shape");
 }
 
 template <typename C>
@@ -1017,15 +1035,8 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   if constexpr (std::is_same<C, float2>::value) {
     const AxisT<C> ax = p->ax2.dev_s(narrow);
-    if (cols_warp_supported(p, narrow ? p->ax2.s8 : p->ax2.s)) {
-      // one warp per column line, 8 lines per CTA
-      LaunchShape shw;
-      shw.TR = 8;
-      shw.threads = 256;
-      shw.smem = 0;
-      const unsigned gw = (unsigned)((G.rows + 7) / 8);
-      return launch_pass<C>(cols_warp_kernel<8>, KIND_COLS, gw, shw, st, G, ax, io);
-    }
+    const AxisPrec& ap = narrow ? p->ax2.s8 : p->ax2.s;
+    if (cols_warp_supported(p, ap)) return launch_cols_warp<BandMulAdd>(p, ap, G, st, ax, io, BandMulAdd{});
     KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
   } else {
     const AxisT<C> ax = p->ax2.dev<C>();
@@ -1559,6 +1570,8 @@ static int launch_cols_admm_split(const bccb_plan_s* p, int batch, const Workspa
   io.K1 = p->ax1.K;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   const AxisT<float2> ax = p->ax2.dev_s(narrow);
+  const AxisPrec& ap = narrow ? p->ax2.s8 : p->ax2.s;
+  if (cols_warp_supported(p, ap)) return launch_cols_warp<AdmmSplitBand>(p, ap, G, st, ax, io, op);
   KP_DISPATCH_F(ax.KP, return launch_pass<float2>(cols_admm_split_kernel<KPC>, KIND_COLS, grid, sh, st, G, ax, io, op));
   return BCCB_OK;
 }

@@ -362,85 +362,105 @@ __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT
   cols_block<KP>(G, ax, io, row0, G.TR, reinterpret_cast<C*>(smem_raw), BandMulAdd{}, pre);
 }
 
-// Warp-per-line column pass (complex64 streaming axis with R = 32 threads per line and a band of
-// K = 32: config 2's L2 = 256 with KP = 8).  The level-2 sums run across the warp instead of
-// through shared memory: each lane forms its 32 twiddled products T_s[j] w_32^{s m}, a
-// recursive-halving reduce-scatter over the 32 lanes leaves band value o = j + KP m on lane o,
-// the band stage Y = D X + P Bh runs on that lane, and 32 shuffles broadcast the band back for
-// the inverse.  No shared memory and no block barrier: a line's latency chain is one warp's.
-// Same arithmetic per term as cols_block (fp32, products then sums; only the summation order
-// of the 32 lanes differs).
-template <int KP>
-__global__ void __launch_bounds__(256) cols_warp_kernel(Geo G, AxisT<float2> ax, ColsIO<float2> io) {
-  constexpr int R = 32, K = 32, MO = K / KP;
-  static_assert(KP * MO == K, "band of 32");
+// Warp-per-line column pass (complex64 streaming axis with R = 32 threads per line and a band
+// of K = 32 NSET: config 2's L2 = 256 with KP = 8, the split ADMM's L2 = 512 with KP = 16 and
+// K = 64).  The level-2 sums run across the warp instead of through shared memory: each lane
+// forms its twiddled products T_s[j] w_32^{s m}; per set of 32 band values a recursive-halving
+// reduce-scatter over the 32 lanes leaves band value 32 set + lane on the lane, the band stage
+// (D X + P Bh, or the split ADMM's float64 box update Op) runs there, and shuffles broadcast the
+// band back for the inverse.  No shared memory and no block barrier: a line's latency chain is
+// one warp's.  Same arithmetic per term as cols_block (fp32 products, then sums; only the
+// summation order over the 32 lanes differs).
+template <int KP, int NSET, typename Op = BandMulAdd>
+__global__ void __launch_bounds__(256) cols_warp_kernel(Geo G, AxisT<float2> ax, ColsIO<float2> io, Op op) {
+  constexpr int R = 32, K = 32 * NSET, MO = K / KP;
+  constexpr bool MULADD = std::is_same<Op, BandMulAdd>::value;
+  static_assert(KP * MO == K, "band");
   const int lane = threadIdx.x & 31;
   const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const bool live = line < G.rows;
-  // loop-invariant operands (before the grid-dependency wait): twiddles and the lane's band
-  // multipliers D[k1][lane], P Bh[line][lane]
+  // loop-invariant operands (before the grid-dependency wait): twiddles and, for D X + P Bh,
+  // the lane's band multipliers D[k1][o], P Bh[line][o]
   float2 tw1[KP], tw2[MO];
 #pragma unroll
   for (int j = 0; j < KP; ++j) tw1[j] = __ldg(ax.tw1 + j * R + lane);
 #pragma unroll
   for (int m = 0; m < MO; ++m) tw2[m] = __ldg(ax.tw2 + m * R + lane);
-  float2 d = make_float2(1.f, 0.f), pb = make_float2(0.f, 0.f);
-  if (live) {
-    const long long k1 = line % io.K1;
-    if (io.D) d = __ldg(io.D + k1 * K + lane);
-    if (io.Bh) {
-      pb = io.Bh[line * K + lane];
-      if (io.P) pb = cmul(pb, __ldg(io.P + k1 * K + lane));
+  float2 d[NSET], pb[NSET];
+#pragma unroll
+  for (int q = 0; q < NSET; ++q) {
+    d[q] = make_float2(1.f, 0.f);
+    pb[q] = make_float2(0.f, 0.f);
+    if (MULADD && live) {
+      const long long k1 = line % io.K1;
+      const int o = 32 * q + lane;
+      if (io.D) d[q] = __ldg(io.D + k1 * K + o);
+      if (io.Bh) {
+        pb[q] = io.Bh[line * K + o];
+        if (io.P) pb[q] = cmul(pb[q], __ldg(io.P + k1 * K + o));
+      }
     }
   }
   pdl_wait();
   if (!live) return;   // whole warps only
   const int N = ax.N;
-  float2 y = make_float2(0.f, 0.f);
+  float2 x[NSET];
+#pragma unroll
+  for (int q = 0; q < NSET; ++q) x[q] = make_float2(0.f, 0.f);
   if (G.do_fwd) {
-    float2 a[KP];
+    float2 t[KP];
     const float2* src = io.U + line * N + lane;
 #pragma unroll
-    for (int r = 0; r < KP; ++r) a[r] = __ldcg(src + R * r);
-    reg_dft<KP, false>(a);
-    float2 v[K];   // v[j + KP m] = a_j w_N^{s j} w_32^{s m}
+    for (int r = 0; r < KP; ++r) t[r] = __ldcg(src + R * r);
+    reg_dft<KP, false>(t);
 #pragma unroll
-    for (int j = 0; j < KP; ++j) {
-      const float2 t = cmul(a[j], tw1[j]);
-      v[j] = t;
+    for (int j = 0; j < KP; ++j) t[j] = cmul(t[j], tw1[j]);
 #pragma unroll
-      for (int m = 1; m < MO; ++m) v[j + KP * m] = cmul(t, tw2[m]);
-    }
-    // reduce-scatter: after the stage of width h the lane keeps the half its bit h selects
+    for (int q = 0; q < NSET; ++q) {
+      float2 v[32];   // v[i]: band value o = 32 q + i = j + KP m
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
-      const bool upper = (lane & h) != 0;
-#pragma unroll
-      for (int i = 0; i < h; ++i) {
-        const float2 send = upper ? v[i] : v[i + h];
-        const float2 keep = upper ? v[i + h] : v[i];
-        const float2 recv = make_float2(__shfl_xor_sync(0xffffffffu, send.x, h),
-                                        __shfl_xor_sync(0xffffffffu, send.y, h));
-        v[i] = cadd(keep, recv);
+      for (int i = 0; i < 32; ++i) {
+        const int o = 32 * q + i, j = o % KP, m = o / KP;
+        v[i] = m == 0 ? t[j] : cmul(t[j], tw2[m]);
       }
+      // reduce-scatter: after the stage of width h the lane keeps the half its bit h selects
+#pragma unroll
+      for (int h = 16; h >= 1; h >>= 1) {
+        const bool upper = (lane & h) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+          const float2 send = upper ? v[i] : v[i + h];
+          const float2 keep = upper ? v[i + h] : v[i];
+          const float2 recv = make_float2(__shfl_xor_sync(0xffffffffu, send.x, h),
+                                          __shfl_xor_sync(0xffffffffu, send.y, h));
+          v[i] = cadd(keep, recv);
+        }
+      }
+      x[q] = v[0];
     }
-    y = io.D ? cmul(v[0], d) : v[0];
   }
-  if (io.Bh) y = cadd(y, pb);
-  if (!G.do_inv) {
-    io.box_out[line * K + lane] = y;
-    return;
+  float2 y[NSET];
+#pragma unroll
+  for (int q = 0; q < NSET; ++q) {
+    if constexpr (MULADD) {
+      y[q] = (G.do_fwd && io.D) ? cmul(x[q], d[q]) : x[q];
+      if (io.Bh) y[q] = cadd(y[q], pb[q]);
+      if (!G.do_inv) io.box_out[line * K + 32 * q + lane] = y[q];
+    } else {
+      y[q] = op(line, 32 * q + lane, x[q]);
+    }
   }
+  if (!G.do_inv) return;
   // inverse: g_j = IDFT_KP( conj(w_N^{s j}) sum_m Y[j + KP m] conj(w_32^{s m}) )
   float2 g[KP];
 #pragma unroll
   for (int j = 0; j < KP; ++j) {
-    g[j] = make_float2(__shfl_sync(0xffffffffu, y.x, j), __shfl_sync(0xffffffffu, y.y, j));
 #pragma unroll
-    for (int m = 1; m < MO; ++m) {
-      const float2 ym = make_float2(__shfl_sync(0xffffffffu, y.x, j + KP * m),
-                                    __shfl_sync(0xffffffffu, y.y, j + KP * m));
-      g[j] = cadd(g[j], cmulc(ym, tw2[m]));
+    for (int m = 0; m < MO; ++m) {
+      const int o = j + KP * m;
+      const float2 ym = make_float2(__shfl_sync(0xffffffffu, y[o / 32].x, o % 32),
+                                    __shfl_sync(0xffffffffu, y[o / 32].y, o % 32));
+      g[j] = m == 0 ? ym : cadd(g[j], cmulc(ym, tw2[m]));
     }
     g[j] = cmulc(g[j], tw1[j]);
   }
