@@ -27,7 +27,7 @@ cap() {  # name cfg kernel-regex skip
 }
 cap cfg2_rows_early 2 rows_fista_fast 9
 cap cfg2_rows_late 2 rows_fista_fast 1500
-cap cfg2_cols_late 2 cols_kernel 1500
+cap cfg2_cols_late 2 cols_warp_kernel 1500
 cap cfg3_rows 3 rows_admm_split 600
 cap cfg4_rows 4 rows_fista_fast 600
 cap cfg5_rows 5 rows_fista_fast 600
