@@ -84,3 +84,46 @@ def test_trial_estimates_match_reference_fast_backend():
             assert not np.asarray(est).any()
         else:
             assert np.linalg.norm(est - ref) / np.linalg.norm(ref) < 1e-4
+
+
+def _tiny_problem():
+    import torch
+    from oracle import bccb_oracle as orc
+    from paper_2509_13592_b200.arrays import make_ura, subsample_preserving_aperture, synthesize_snapshot, Target
+    geom = subsample_preserving_aperture(make_ura(6, 4), 14, seed=4)
+    l1, l2 = 8, 4
+    y = synthesize_snapshot(geom, [Target(-0.25, 0.0, 1.5 - 0.5j), Target(0.125, -0.25, 1j)], 0.05, seed=104)
+    a = ex._dictionary_rows(geom, l1, l2, torch.device("cpu"))
+    m1, m2 = geom.occupied_coordinates()
+    np.testing.assert_array_equal(a.numpy(), orc.dictionary_matrix(m1, m2, l1, l2))
+    b = a.conj().T @ torch.as_tensor(y)
+    return geom, l1, l2, a, b, orc
+
+
+def test_regular_column_loops_match_oracle_on_cpu_tensors():
+    """The harness's dense regular column (run on the GPU in the sweep) restates the reference's
+    regular backend: its Gram and ISTA loop, on CPU tensors, against the pinned oracle."""
+    import torch
+    geom, l1, l2, a, b, orc = _tiny_problem()
+    bn = b.numpy()
+    tau = 0.1 * float(np.abs(bn).max())
+    mu = 1.0 / 32.0
+    gram = orc.dense_gram(*geom.occupied_coordinates(), l1, l2)
+    op = a.conj().T @ a
+    np.testing.assert_allclose(op.numpy(), gram, rtol=0, atol=1e-12)
+    c = torch.zeros_like(b)
+    for _ in range(40):
+        c = ex._soft(c - mu * (op @ c) + mu * b, mu * tau)
+    ref = orc.ista_dense(gram, bn, tau, mu, 40)
+    assert np.linalg.norm(c.numpy() - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_bccb_deviation_on_cpu_tensors():
+    import torch
+    from paper_2509_13592_b200.cli import _bccb_deviation
+    geom, l1, l2, a, b, orc = _tiny_problem()
+    dense = a.conj().T @ a
+    assert _bccb_deviation(dense, l1, l2) < 1e-12
+    broken = dense.clone()
+    broken[3, 5] += 1e-3
+    assert _bccb_deviation(broken, l1, l2) >= 1e-3 * 0.999
