@@ -199,3 +199,46 @@ def test_substream_split_is_bitwise_neutral(substreams):
     from paper_2509_13592_b200.solvers import admm_solve_with_c
     z = substreams(3, lambda: admm_solve_with_c(bb.LassoProblem.from_measurements(op3, y32, tau=taus3), conf3)[0])
     np.testing.assert_array_equal(z.cpu().numpy(), outs[0])
+
+
+_PDL_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2509_13592_b200 as bb
+from paper_2509_13592_b200 import scenes
+from oracle import bccb_oracle as orc
+w = scenes.workload(2)
+geom, ys, _ = scenes.make_scene(w, range(9))
+op = bb.gram_operator(geom, w.l1, w.l2)
+m1, m2 = geom.occupied_coordinates()
+bs = np.stack([orc.adjoint_fft(m1, m2, w.l1, w.l2, y) for y in ys])
+taus = np.array([w.tau_fraction * np.abs(b).max() for b in bs])
+est = bb.fista_solve(bb.LassoProblem(op, bs, taus), bb.SolverConfig(iterations=120, step_size_mu=1.0 / (w.l1 * w.l2))).estimate
+np.save(sys.argv[2], est)
+"""
+
+
+@pytest.mark.parametrize("env,bitwise", [({"BCCB_PDL": "0"}, True), ({"BCCB_PDL": "2"}, True),
+                                         ({"BCCB_COLS_WARP": "0"}, False)])
+def test_launch_modes_agree(tmp_path, env, bitwise):
+    """Programmatic dependent launch (with early reads before the grid-dependency wait) must not
+    change a bit: default (PDL with early release) vs PDL off / implicit release, each in a fresh
+    process (the modes are read once).  The warp-per-line column pass sums the band in a
+    different order than the shared-memory pass: equal to rounding."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(_PDL_SCRIPT)
+    outs = []
+    for extra in ({}, env):
+        out = tmp_path / f"est{len(outs)}.npy"
+        e = dict(os.environ, **extra)
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=e, timeout=600)
+        outs.append(np.load(out))
+    if bitwise:
+        np.testing.assert_array_equal(outs[0], outs[1])
+    else:
+        for a, b in zip(outs[0], outs[1]):
+            assert orc.rel_l2(a, b) < 1e-6
