@@ -2,7 +2,7 @@
 and iteration count through the public API, with a sample of snapshots re-solved by the pinned
 float64 CPU oracle (oracle/bccb_oracle.py) in a process pool on the host cores.
 
-    python tools/parity_full.py OUT.json [--cfg5-iterations T]
+    python tools/parity_full.py OUT.json [--cfg5-iterations T] [--only 2,5]
 
 Writes rel-L2 (GPU estimate vs oracle) and top-K index-set agreement per checked snapshot.
 Config 3 compares c and v (the reference's z is identically zero there, SURVEY finding 7).
@@ -44,6 +44,7 @@ def _oracle(args):
 def main():
     out_path = sys.argv[1]
     t5 = int(sys.argv[sys.argv.index("--cfg5-iterations") + 1]) if "--cfg5-iterations" in sys.argv else None
+    only = {int(c) for c in sys.argv[sys.argv.index("--only") + 1].split(",")} if "--only" in sys.argv else None
     import torch
     import paper_2509_13592_b200 as bb
     from oracle import bccb_oracle as orc
@@ -51,6 +52,8 @@ def main():
     from paper_2509_13592_b200.solvers import admm_solve_with_c
     jobs, gpu = [], {}
     for cfg, snaps in PLAN.items():
+        if only and cfg not in only:
+            continue
         w = scenes.workload(cfg)
         T = t5 if (cfg == 5 and t5) else w.iterations
         geom, ys, _ = scenes.make_scene(w)
