@@ -1251,7 +1251,8 @@ static int sub_batches(const bccb_plan_s* p, int batch) {
   int n = g_substreams.load();
   if (n < 0) {
     const char* e = getenv("BCCB_SUBSTREAMS");
-    n = e ? atoi(e) : 3;   // measured best at config 2 with PDL (2: 171, 3: 186, 4: 177 G gpi/s)
+    n = e ? atoi(e) : 3;   // measured best at config 2 with PDL (2: 171, 3: 186, 4: 177 G gpi/s;
+                          // with the warp column pass 2: 202.1, 3: 202.5, 4: 196.5, 5: 179.4)
   }
   n = std::max(1, std::min(n, bccb_plan_s::MAX_SUB));
   while (n > 1 && (batch < n || (long long)(batch / n) * p->L2 < 2048)) --n;
