@@ -4,5 +4,5 @@ for cfg in "$@"; do
 import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']
 print('cfg$cfg', round(d['value']/1e9,2), 'Ggpi/s', round(d['ms_per_step'],3), 'ms', 'launch/step', d['gpu_launches_per_step'],
       'rows_ms', round(r['avg_launch_ms'],4), 'rows_share', round(r['share_of_step'],3),
-      'cols', {k: round(v,4) for k,v in (r.get('cols_kernel') or {}).items()})"
+      'cols', {k: (round(v,4) if isinstance(v,(int,float)) else v) for k,v in (r.get('cols_kernel') or {}).items()})"
 done
