@@ -851,6 +851,12 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   // tile's U band may be nonzero; clear = U already holds zeros, the store can be skipped)
   unsigned* fw = ZS ? flags + ((long long)tile * (NT / 32 + 1) + (tid >> 5)) : nullptr;
   unsigned* tword = ZS ? flags + ((long long)tile * (NT / 32 + 1) + NT / 32) : nullptr;
+  // Reads before the dependency wait are safe only when a separate column pass runs between
+  // two rows passes (it waited for the previous rows pass).  With the fused column pass
+  // (KP2 > 0) the previous grid on the stream IS the previous rows pass, still writing the
+  // flags and the state when PDL releases this grid, so everything waits first.
+  constexpr bool PRE_WAIT_READS = KP2 == 0;
+  if constexpr (!PRE_WAIT_READS) pdl_wait();
   const unsigned fl = ZS ? __ldcg(fw) : 0xffffffffu;
   const unsigned u_maybe_nonzero = ZS ? __ldcg(tword) : 1u;
   bool warp_zero = false;   // the whole warp's next operator input is zero
@@ -864,13 +870,13 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   // this grid's own dependency wait; the band tile V comes from that column pass (after it).
   // Early only for short lines (config 2: +2.7%); the long-line shapes keep the load order
   // band tile -> state (configs 4/5 measured 1-2% slower with the state first).
-  constexpr bool EARLY = R <= 16;
+  constexpr bool EARLY = PRE_WAIT_READS && R <= 16;
   St sb[CH];
   if (EARLY && G.do_inv) {
 #pragma unroll
     for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
   }
-  pdl_wait();
+  if constexpr (PRE_WAIT_READS) pdl_wait();
   if (G.do_inv) {
     // band tile V[b][k][l20 + ii] -> Xs[ii][k]
     for (int idx = tid; idx < TR * K; idx += NT) {

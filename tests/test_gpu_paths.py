@@ -207,7 +207,7 @@ sys.path.insert(0, sys.argv[1])
 import paper_2509_13592_b200 as bb
 from paper_2509_13592_b200 import scenes
 from oracle import bccb_oracle as orc
-w = scenes.workload(2)
+w = scenes.workload(int(sys.argv[3]))
 geom, ys, _ = scenes.make_scene(w, range(9))
 op = bb.gram_operator(geom, w.l1, w.l2)
 m1, m2 = geom.occupied_coordinates()
@@ -235,10 +235,43 @@ def test_launch_modes_agree(tmp_path, env, bitwise):
     for extra in ({}, env):
         out = tmp_path / f"est{len(outs)}.npy"
         e = dict(os.environ, **extra)
-        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=e, timeout=600)
+        subprocess.run([sys.executable, str(script), root, str(out), "2"], check=True, env=e, timeout=600)
         outs.append(np.load(out))
     if bitwise:
         np.testing.assert_array_equal(outs[0], outs[1])
     else:
         for a, b in zip(outs[0], outs[1]):
             assert orc.rel_l2(a, b) < 1e-6
+
+
+@pytest.mark.parametrize("pdl", ["1", "0"])
+def test_fused_column_pass_pdl(tmp_path, pdl):
+    """The fused column pass (rows kernel whose last CTA per snapshot runs the column pass; taken
+    at L1 = 64 when the cluster and small-grid solvers are off) has no separate column pass
+    between two rows passes, so nothing may be read before the grid-dependency wait: with PDL on
+    it must agree bitwise with PDL off and match the float64 oracle (config-1 geometry, 9
+    snapshots, fresh processes)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(_PDL_SCRIPT)
+    outs = []
+    for extra in ({"BCCB_CLUSTER": "0", "BCCB_SMALL_GRID": "0", "BCCB_PDL": pdl},
+                  {"BCCB_CLUSTER": "0", "BCCB_SMALL_GRID": "0", "BCCB_PDL": "0"}):
+        out = tmp_path / f"est{len(outs)}.npy"
+        e = dict(os.environ, **extra)
+        subprocess.run([sys.executable, str(script), root, str(out), "1"], check=True, env=e, timeout=600)
+        outs.append(np.load(out))
+    assert np.isfinite(outs[0]).all() and np.count_nonzero(outs[0]) > 0
+    np.testing.assert_array_equal(outs[0], outs[1])
+    w = scenes.workload(1)
+    geom, ys, _ = scenes.make_scene(w, range(9))
+    m1, m2 = geom.occupied_coordinates()
+    eig_t = np.ascontiguousarray(orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2).T)
+    mu = 1.0 / (w.l1 * w.l2)
+    for s_, y in enumerate(ys[:3]):
+        b = orc.adjoint_fft(m1, m2, w.l1, w.l2, y)
+        ref = orc.fista(eig_t, b, w.tau_fraction * np.abs(b).max(), mu, 120)
+        assert orc.rel_l2(outs[0][s_], ref) < 1e-4
