@@ -116,11 +116,12 @@ extern "C" const char* bccb_version(void) { return "bccb_b200 0.1.0 (sm_100a)"; 
 // ------------------------------------------------------------------ launch mode
 // Programmatic dependent launch of the pass kernels (BCCB_PDL): 0 off, 1 on with each CTA
 // releasing its dependents right after its griddepcontrol.wait, 2 on with the implicit
-// release at grid completion.
+// release at grid completion (default: measured +0.6 % at config 2, +0.3 % at config 3,
+// neutral at configs 4/5 against mode 1, profiles/ab/r1_pdl_modes.txt).
 static int pdl_mode() {
   static const int m = [] {
     const char* e = getenv("BCCB_PDL");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   return m;
 }

@@ -226,11 +226,12 @@ np.save(sys.argv[2], est)
 """
 
 
-@pytest.mark.parametrize("env,bitwise", [({"BCCB_PDL": "0"}, True), ({"BCCB_PDL": "2"}, True),
+@pytest.mark.parametrize("env,bitwise", [({"BCCB_PDL": "0"}, True), ({"BCCB_PDL": "1"}, True),
+                                         ({"BCCB_PDL": "2"}, True),
                                          ({"BCCB_COLS_WARP": "0"}, False)])
 def test_launch_modes_agree(tmp_path, env, bitwise):
     """Programmatic dependent launch (with early reads before the grid-dependency wait) must not
-    change a bit: default (PDL with early release) vs PDL off / implicit release, each in a fresh
+    change a bit: default (PDL, implicit release at grid completion) vs PDL off / early release, each in a fresh
     process (the modes are read once).  The warp-per-line column pass sums the band in a
     different order than the shared-memory pass: equal to rounding."""
     import os
@@ -287,7 +288,7 @@ def test_fused_column_pass_pdl(tmp_path, pdl):
 
 @pytest.mark.parametrize("cfg,solver,iters", [(3, "admm", 120), (2, "ista", 120), (4, "fista", 120), (1, "fista", 120)])
 def test_pdl_bitwise_across_solvers(tmp_path, cfg, solver, iters):
-    """PDL on (default, early release) vs off must agree bitwise for every solver's default
+    """PDL on (early release, mode 1; implicit release, the default) vs off must agree bitwise for every solver's default
     kernel path: a read placed before the grid-dependency wait that races the preceding pass
     shows up here as a difference (9 snapshots, fresh processes; ADMM compares z, v and c:
     z stays zero at rho = 1 on the config-3 scene)."""
@@ -298,11 +299,12 @@ def test_pdl_bitwise_across_solvers(tmp_path, cfg, solver, iters):
     script = tmp_path / "run.py"
     script.write_text(_PDL_SCRIPT)
     outs = []
-    for extra in ({}, {"BCCB_PDL": "0"}):
+    for extra in ({"BCCB_PDL": "1"}, {}, {"BCCB_PDL": "0"}):
         out = tmp_path / f"est{len(outs)}.npy"
         e = dict(os.environ, **extra)
         subprocess.run([sys.executable, str(script), root, str(out), str(cfg), solver, str(iters)], check=True, env=e,
                        timeout=600)
         outs.append(np.load(out))
     assert np.isfinite(outs[0]).all() and np.count_nonzero(outs[0]) > 0
-    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
+    np.testing.assert_array_equal(outs[1], outs[2])
