@@ -1252,7 +1252,10 @@ static int sub_batches(const bccb_plan_s* p, int batch) {
   int n = g_substreams.load();
   if (n < 0) {
     const char* e = getenv("BCCB_SUBSTREAMS");
-    n = e ? atoi(e) : 3;   // measured best at config 2 with PDL (2: 171, 3: 186, 4: 177 G gpi/s;
+    // short lines (L1 <= 256) are latency-bound: four sub-batches (config 2 with PDL mode 2:
+    // 3: 204.2, 4: 204.9 G gpi/s); longer lines keep three (config 4: 297.4 vs 296.9, config 3
+    // ADMM: 299.6 vs 298.3; profiles/ab/r1_substreams_pdl2.txt).  Earlier (PDL mode 1):
+    n = e ? atoi(e) : (p->L1 <= 256 ? 4 : 3);   // measured at config 2 (2: 171, 3: 186, 4: 177 G gpi/s;
                           // with the warp column pass 2: 202.1, 3: 202.5, 4: 196.5, 5: 179.4)
   }
   n = std::max(1, std::min(n, bccb_plan_s::MAX_SUB));
