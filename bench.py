@@ -1,17 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the fused BCCB-FISTA hot path (BASELINE.json metric, grid-point-iterations/s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl b200|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
 
-A step = one full solve (T solver iterations) over this rank's batch of snapshots.
-Default workload = BASELINE config 2 (configs[1], the metric's configuration):
-FISTA, 64 snapshots per GPU, L1 = L2 = 256, T = 1000 (weak scaling: every rank
-solves its own 64 snapshots).  `value` times the device-resident solve loop with
-CUDA events (max over ranks); `e2e` times the public API end to end with host
-(pinned) buffers: H2D of y, GPU adjoint, solve, top-K, D2H of spectra + peaks.
---impl reference times the reference algorithm (the pinned CPU oracle port,
-oracle/bccb_oracle.py) on this host's cores.
+A step = one full solve (T solver iterations) over this rank's shard of snapshots.
+Default workload = BASELINE config 5 (configs[4]), the largest single-GPU configuration
+and the one north_star's "fused FISTA iteration" target is quoted on: FISTA, batch 32,
+L1 = L2 = 4096, T = 1000.  Configs 4 and 5 are strong-scaled like BASELINE states ("batch
+sharded across 1/2/4/8 GPUs": rank r solves shard_bounds(B, r, N)); configs 1-3 are weak-
+scaled (every rank solves its own batch).  `value` times the device-resident solve with
+CUDA events (max over ranks); `e2e` times the public API end to end with host (pinned)
+buffers on every rank: H2D of y, GPU adjoint, solve, top-K, then one grouped NCCL
+send/recv gather of spectra + peaks to rank 0 and its D2H, timed with CUDA events on the
+launching stream (max over ranks).  --impl reference times the reference algorithm (the
+pinned CPU oracle port, oracle/bccb_oracle.py) on this host's cores; it maps no CUDA
+library of this repo (the package loads libbccb_b200.so lazily).
 """
 
 import argparse
@@ -41,15 +45,25 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--iterations", type=int, default=None, help="override T (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--substreams", type=int, default=0, help="sub-batch streams (0: library default)")
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="do not bracket each launch of the timed steps with CUDA events")
     return ap.parse_args()
 
 
+# BASELINE.json configs 4 and 5: "batch ... sharded across 1/2/4/8 GPUs" (strong scaling)
+STRONG = (4, 5)
+
+
 # ----------------------------------------------------------------------------- CPU leg
+
+_CPU_CACHE = {}
+
 
 def _cpu_worker(args):
     cfg, snap, iters = args
@@ -57,11 +71,18 @@ def _cpu_worker(args):
     from oracle import bccb_oracle as orc
     from paper_2509_13592_b200 import scenes
     w = scenes.workload(cfg)
-    geom, ys, _ = scenes.make_scene(w, [snap])
-    m1, m2 = geom.occupied_coordinates()
-    eig = orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2)
-    b = orc.adjoint_fft(m1, m2, w.l1, w.l2, ys[0])
-    tau = w.tau_fraction * float(np.max(np.abs(b)))
+    # untimed precompute (like SolverResult.total_seconds, solvers.py:271-278), cached per
+    # worker process: the shared spectrum once per config, b for the last snapshot seen
+    if _CPU_CACHE.get("cfg") != cfg:
+        _CPU_CACHE.clear()
+        geom = scenes.geometry_for(w)
+        _CPU_CACHE.update(cfg=cfg, geom=geom, eig=orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2))
+    if _CPU_CACHE.get("snap") != snap:
+        geom, ys, _ = scenes.make_scene(w, [snap])
+        m1, m2 = geom.occupied_coordinates()
+        b = orc.adjoint_fft(m1, m2, w.l1, w.l2, ys[0])
+        _CPU_CACHE.update(snap=snap, b=b, tau=w.tau_fraction * float(np.max(np.abs(b))))
+    eig, b, tau = _CPU_CACHE["eig"], _CPU_CACHE["b"], _CPU_CACHE["tau"]
     t0 = time.perf_counter()
     if w.solver == "admm":
         orc.admm(eig, b, tau, w.rho, iters)
@@ -160,7 +181,7 @@ def run_reference(args, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "scaling": scaling_of(w), "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": workload_config(w, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -169,14 +190,22 @@ def run_reference(args, rank):
 
 
 def workload_config(w, n):
+    strong = w.cfg in STRONG
+    per_gpu = f"{w.batch} snapshots sharded over {n} GPU(s)" if strong else f"{w.batch} snapshots/GPU"
     return {
-        "workload": (f"cfg{w.cfg}: {w.solver.upper()}, {w.batch} snapshots/GPU, {w.m1}x{w.m2} URA with "
+        "workload": (f"cfg{w.cfg}: {w.solver.upper()}, {per_gpu}, {w.m1}x{w.m2} URA with "
                      f"{w.elements} elements, L1={w.l1} L2={w.l2}, T={w.iterations}, K={w.targets} targets, "
                      f"{w.snr_db:g} dB, tau={w.tau_fraction:g} max|A^H y|"),
-        "batch_per_gpu": w.batch, "global_batch": w.batch * n, "l1": w.l1, "l2": w.l2,
-        "iterations": w.iterations, "parallelism": f"dp{n} (snapshot shards, no per-iteration comm)",
-        "l2_cache": "flushed between steps (256 MiB write)",
+        "global_batch": w.batch if strong else w.batch * n,
+        "batch_per_gpu": (-(-w.batch // n)) if strong else w.batch,
+        "l1": w.l1, "l2": w.l2, "iterations": w.iterations,
+        "parallelism": f"dp{n} (snapshot shards, no per-iteration comm; rank-0 gather after the loop)",
+        "l2_cache": "flushed between steps (256 MiB write); the iterate state exceeds L2",
     }
+
+
+def scaling_of(w):
+    return "strong" if w.cfg in STRONG else "weak"
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -223,6 +252,83 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- GPU leg
 
+FP32_LANES_PER_SM = 128       # B200 (sm_100a): 4 SMSPs x 32 FP32 lanes
+B200_SMS = 148
+
+
+def ncu_summary(cfg):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        return json.load(open(path)).get(f"cfg{cfg}", {})
+    except Exception:
+        return {}
+
+
+def build_roofline(w, T, B, value_per_gpu, rows_ms, n_rows, kern_ms_total, step_ms_total, cols, clk):
+    """Roofline of the dominant kernel (the rows pass), against the bound that binds.
+
+    The band-pruned, sparsity-skipping rows pass is FP32-issue bound (profiles/: sm__throughput
+    56-65 %, FADD+FFMA+FMUL ~70 % of instructions, DRAM 0.7-1.9 B/gpi), so the roofline is
+    FP32 flops per launch / launch time against 148 SMs x 128 lanes x 2 flops x the SM clock
+    measured during the timed region.  Flops per grid-point-iteration of the rows kernel come
+    from the ncu launch list of one full solve of the same code (profiles/ncu_summary.json:
+    sm__sass_thread_inst_executed_op_{fadd,fmul,ffma}_pred_on.sum, FFMA counted twice); DRAM
+    traffic per launch from the same list.  SURVEY 8(d)'s dense 80 B/gpi model is reported only
+    as "effective_bandwidth" (band pruning makes the kernel move ~1 B/gpi)."""
+    summ = ncu_summary(w.cfg)
+    L = w.l1 * w.l2
+    iters_per_launch = T * B / max(n_rows, 1) / B      # ~1 for per-pass kernels, T for whole-solve kernels
+    gpi_per_launch = B * L * T / max(n_rows, 1)
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    fp32_peak = B200_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12       # TFLOP/s
+    flops_gpi = summ.get("rows_fp32_flops_per_gpi")
+    inst_gpi = summ.get("rows_warp_inst_per_gpi")
+    dram_gpi = summ.get("rows_dram_bytes_per_gpi")
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured (MEASURED_PEAKS.json copy test)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    launch_s = rows_ms / 1e3
+    r = {"kernel": f"rows_{w.solver}_kernel (band IFFT + fused prox/momentum epilogue + band FFT)",
+         "avg_launch_ms": rows_ms, "launches_per_step": n_rows,
+         "gpi_per_launch": gpi_per_launch, "iterations_per_launch": iters_per_launch,
+         "share_of_step": kern_ms_total / step_ms_total if step_ms_total else None,
+         "launch_timing": "CUDA events around every launch of the timed steps, on the launch's stream"}
+    if flops_gpi:
+        achieved = flops_gpi * gpi_per_launch / launch_s / 1e12
+        r.update({"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                  "frac": achieved / fp32_peak,
+                  "flops_per_launch": flops_gpi * gpi_per_launch,
+                  "flops_per_gpi": flops_gpi,
+                  "flops_source": summ.get("source"),
+                  "peak_source": f"{B200_SMS} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_mhz:.0f} MHz "
+                                 "(SM clock measured during the timed region)"})
+    else:
+        r.update({"bound": "fp32", "achieved": None, "peak": fp32_peak, "unit": "TFLOP/s", "frac": None,
+                  "flops_source": "profiles/ncu_summary.json has no FP32 count for this config"})
+    r["traffic"] = dram_gpi * gpi_per_launch if dram_gpi is not None else None
+    r["traffic_note"] = "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (full-solve average)"
+    if inst_gpi:
+        ipc_peak = 4 * B200_SMS * sm_mhz * 1e6                  # one warp-instruction per SMSP per clock
+        ach = inst_gpi * gpi_per_launch / launch_s
+        r["issue"] = {"warp_inst_per_gpi": inst_gpi, "achieved_warp_inst_per_s": ach, "peak": ipc_peak,
+                      "frac": ach / ipc_peak}
+    if dram_gpi is not None:
+        r["hbm"] = {"achieved_gbs": dram_gpi * gpi_per_launch / launch_s / 1e9, "peak_gbs": hbm_peak,
+                    "frac": dram_gpi * gpi_per_launch / launch_s / 1e9 / hbm_peak, "peak_source": hbm_src}
+    dense = summ.get("dense_phase")
+    if dense:
+        r["hbm_dense_phase"] = dense | {"frac": dense["gbs"] / hbm_peak, "peak_gbs": hbm_peak}
+    eff = B_ALG[w.solver] * value_per_gpu / 1e9
+    r["effective_bandwidth"] = {"bytes_per_gpi": B_ALG[w.solver], "gbs": eff, "of_hbm_peak": eff / hbm_peak,
+                                "note": "SURVEY 8(d) dense 'FFT sweeps x 8 B' model x measured gpi/s: "
+                                        "an effective figure, not a roofline (band pruning + sparsity "
+                                        "skipping move ~1 B/gpi)"}
+    if cols:
+        r["cols_kernel"] = cols
+    return r
+
+
 def main():
     args = parse()
     from paper_2509_13592_b200 import distributed as bdist
@@ -230,6 +336,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    import ctypes
     import numpy as np
     import torch
     import paper_2509_13592_b200 as bb
@@ -240,9 +347,15 @@ def main():
     torch.cuda.set_device(dev)
     w = scenes.workload(args.config)
     T = args.iterations or w.iterations
-    B = w.batch
-    snaps = range(rank * B, (rank + 1) * B)            # weak scaling: own 64 snapshots per rank
-    geom, y_np, _ = scenes.make_scene(w, snaps)
+    strong = w.cfg in STRONG
+    lo, hi = bdist.workload_shard(w.batch, rank, world, strong)
+    B = hi - lo
+    total = w.batch if strong else w.batch * world
+    if B < 1:
+        raise SystemExit(f"rank {rank}: empty shard ({w.batch} snapshots over {world} ranks)")
+    if args.substreams:
+        _lib.check(_lib.lib.bccb_set_substreams(args.substreams))
+    geom, y_np, _ = scenes.make_scene(w, range(lo, hi))
     op = bb.gram_operator(geom, w.l1, w.l2, device=dev)
     L = op.dimension
     mu = 1.0 / op.max_eigenvalue()
@@ -283,11 +396,16 @@ def main():
     torch.cuda.synchronize(dev)
     assert int(fb.min()) == 2**31 - 1, "non-finite iterate in warm-up"
 
-    # ---- timed region: K steps, CUDA events on the launching stream
+    # ---- timed region: K steps, CUDA events on the launching stream; every library launch is
+    # also bracketed by CUDA events on its own stream (bccb_profile_begin/end) for the roofline
     clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
     times = []
     launches0 = _lib.lib.bccb_launch_count()
+    ms_k = (ctypes.c_double * 3)()
+    n_k = (ctypes.c_longlong * 3)()
+    if not args.no_kernel_events:
+        _lib.lib.bccb_profile_begin()
     for _ in range(args.steps):
         reset()
         barrier()
@@ -300,74 +418,39 @@ def main():
         barrier()
         times.append(e0.elapsed_time(e1))
     launches = _lib.lib.bccb_launch_count() - launches0
+    if not args.no_kernel_events:
+        _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
     clk = clocks.stop()
     ms_local = statistics.mean(times)
     ms_step = bdist.max_over_ranks(ms_local)
     gpi_step = B * L * T
-    value = world * gpi_step / (ms_step / 1e3)
+    value = total * L * T / (ms_step / 1e3)
+    nsub = int(_lib.lib.bccb_substreams_for(op._plan, B))
 
-    # ---- per-kernel live timing: one extra profiled step, single stream (one launch = the whole
-    # batch, no concurrent-stream overlap inside the event brackets), events around every launch
-    reset()
-    torch.cuda.synchronize(dev)
-    _lib.check(_lib.lib.bccb_set_substreams(1))
-    _lib.lib.bccb_profile_begin()
-    run()
-    import ctypes
-    ms_k = (ctypes.c_double * 3)()
-    n_k = (ctypes.c_longlong * 3)()
-    _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
-    _lib.check(_lib.lib.bccb_set_substreams(0))        # back to the library default
-    rows_ms = ms_k[0] / max(n_k[0], 1)
-    cols_ms = ms_k[1] / max(n_k[1], 1)
-    step_kernel_ms = ms_k[0] + ms_k[1] + ms_k[2]
-
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured (MEASURED_PEAKS.json copy test)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    fused_cols = n_k[1] == 0
-    # algorithmic bytes of one launch: the per-iteration model x the iterations the launch
-    # covers (T / launches: ~1 for the per-pass kernels, T for the whole-solve small-grid and
-    # cluster kernels)
-    iters_per_launch = T / max(n_k[0], 1)
-    rows_bytes = (B_ALG_ROWS[w.solver] + (B_ALG_COLS if fused_cols else 0)) * B * L * iters_per_launch
-    achieved = rows_bytes / (rows_ms / 1e3) / 1e9
-    traffic = None
-    ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(ncu_path):
-        try:
-            per_gpi = json.load(open(ncu_path)).get(f"cfg{w.cfg}", {}).get("rows_dram_bytes_per_gpi")
-            traffic = None if per_gpi is None else per_gpi * B * L   # DRAM bytes per (full-batch) launch
-        except Exception:
-            traffic = None
-    iter_achieved = B_ALG[w.solver] * (value / world) / 1e9
-    roofline = {
-        "bound": "hbm", "kernel": f"rows_{w.solver}_kernel (band IFFT + fused epilogue + band FFT)",
-        "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-        "traffic": traffic, "traffic_source": "profiles/ncu_summary.json (ncu dram__bytes_read+write, solve average)",
-        "peak_source": peak_src,
-        "algorithmic_bytes_per_launch": rows_bytes,
-        "bytes_model": (f"{B_ALG_ROWS[w.solver]}{' + 16 (fused K3)' if fused_cols else ''} B/gpi x {B}x{L} gpi "
-                        f"x {iters_per_launch:.4g} iterations per launch (SURVEY 8(d) K4+K2 share)"),
-        "avg_launch_ms": rows_ms, "share_of_step": ms_k[0] / step_kernel_ms,
-        "launch_timing": "profiled extra step, single stream, CUDA events on the launch stream",
-        "cols_kernel": ({"avg_launch_ms": cols_ms, "achieved": B_ALG_COLS * B * L / (cols_ms / 1e3) / 1e9,
-                         "share_of_step": ms_k[1] / step_kernel_ms} if n_k[1] else
-                        {"fused": "column pass runs inside the rows kernel (last CTA per snapshot)"}),
-        "iteration": {"bytes_per_gpi": B_ALG[w.solver], "achieved": iter_achieved,
-                      "frac": iter_achieved / hbm_peak, "frac_vs_8TBs_spec": iter_achieved / 8000.0},
-    }
+    roofline = None
+    if not args.no_kernel_events and n_k[0]:
+        K = args.steps
+        rows_ms = ms_k[0] / n_k[0]
+        cols = None
+        if n_k[1]:
+            cols_ms = ms_k[1] / n_k[1]
+            cols = {"kernel": "cols pass (band FFT . D + P.Bhat . band IFFT)", "avg_launch_ms": cols_ms,
+                    "launches_per_step": n_k[1] // K, "share_of_step": ms_k[1] / (K * ms_local)}
+        roofline = build_roofline(w, T, B, value / world, rows_ms, n_k[0] // K, ms_k[0] / K, ms_local, cols, clk)
+        roofline["substreams"] = nsub
+        if nsub > 1:
+            roofline["launch_timing"] += (f"; {nsub} sub-batch streams run concurrently, so per-launch "
+                                          "durations include time shared with the other streams")
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
         y_host = torch.from_numpy(y_np.astype(np.complex64)).pin_memory()
         k = min(w.targets, 64)
-        # rank 0 receives every rank's spectra and peak lists (one NCCL all-gather after the loop)
-        rows_out = B * world if rank == 0 else B
-        out_host = torch.empty((rows_out, L), dtype=torch.complex64).pin_memory()
-        idx_host = torch.empty((rows_out, k), dtype=torch.int32).pin_memory()
+        out_dev = torch.empty((total, L), dtype=torch.complex64, device=dev) if rank == 0 else None
+        idx_dev = torch.empty((total, k), dtype=torch.int32, device=dev) if rank == 0 else None
+        out_host = torch.empty((total, L), dtype=torch.complex64).pin_memory() if rank == 0 else None
+        idx_host = torch.empty((total, k), dtype=torch.int32).pin_memory() if rank == 0 else None
         cfg = bb.SolverConfig(iterations=T, step_size_mu=mu, rho=w.rho)
         solve = {"ista": bb.ista_solve, "fista": bb.fista_solve, "admm": bb.admm_solve}[w.solver]
 
@@ -377,32 +460,37 @@ def main():
             r = solve(p, cfg)
             est = r.estimate.to(torch.complex64)
             idx, _ = bb.topk_peaks(est, k)
-            if world > 1:
-                est = bdist.gather_rows(est, B * world)
-                idx = bdist.gather_rows(idx, B * world)
-            if est is not None:
+            # rank-0 gather (grouped NCCL send/recv straight into rank 0's output)
+            est = bdist.gather_rows(est, total, out=out_dev)
+            idx = bdist.gather_rows(idx, total, out=idx_dev)
+            if rank == 0:
                 out_host.copy_(est, non_blocking=True)
                 idx_host.copy_(idx, non_blocking=True)
-            torch.cuda.synchronize(dev)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
+        torch.cuda.synchronize(dev)
         et = []
         for _ in range(args.steps):
             flush.fill_(1)
             barrier()
             torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             e2e_step()
-            et.append(time.perf_counter() - t0)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            et.append(e0.elapsed_time(e1))
             barrier()
-        e_s = bdist.max_over_ranks(statistics.mean(et))
-        e2e = {"value": world * gpi_step / e_s, "unit": UNIT, "ms_per_step": e_s * 1e3,
-               "h2d_bytes_per_step": int(world * y_host.numel() * 8),
-               "d2h_bytes_per_step": int(world * B * L * 8 + world * B * k * 4),
-               "path": ("LassoProblem.from_measurements (GPU A^H y) -> solve -> topk_peaks"
-                        + (" -> NCCL all-gather of spectra + peaks to rank 0" if world > 1 else "")
-                        + "; pinned host y in (every rank), complex64 spectra + peak indices out (rank 0)")}
+        e_ms = bdist.max_over_ranks(statistics.mean(et))
+        e2e = {"value": total * L * T / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(total * w.elements * 8),
+               "d2h_bytes_per_step": int(total * L * 8 + total * k * 4),
+               "timing": "CUDA events on the launching stream around the whole step, max over ranks",
+               "path": ("pinned host y -> LassoProblem.from_measurements (GPU A^H y, device tau) -> "
+                        f"{w.solver}_solve -> topk_peaks"
+                        + (" -> grouped NCCL send/recv of spectra + peaks to rank 0" if world > 1 else "")
+                        + " -> complex64 spectra + peak indices D2H (rank 0)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -411,18 +499,19 @@ def main():
         iters = cpu_iters_for(w.cfg, workers)
         pool = _cpu_pool(workers)
         try:
+            cpu_sample(w.cfg, workers, 1, pool)          # untimed: per-worker scene precompute
             v, wall, _ = cpu_sample(w.cfg, workers, iters, pool)
         finally:
             pool.close()
         cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
                "sample": f"oracle {w.solver.upper()} (numpy pocketfft, float64) on {workers} snapshots x {iters} "
-                         f"iterations, one process per core; {wall:.1f} s wall",
+                         f"iterations, one process per core; loop time of the slowest worker; {wall:.1f} s wall",
                "dense": dense_sample(w.cfg)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling_of(w),
             "vs_baseline": None, "dtype": "c64 FFT + f64 iterate", "data": "synthetic (seeded scenes, SURVEY 8(d))",
             "config": workload_config(w, world) | ({"iterations": T} if args.iterations else {}),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -174,6 +174,10 @@ int bccb_profile_end(double* ms_by_kind, long long* launches_by_kind);
  * independent snapshots, so results are bitwise identical either way. */
 int bccb_set_substreams(int n);
 
+/* Sub-batch stream count a solver call on `plan` with this batch would use now (bench:
+ * how many launches of a pass run concurrently). */
+int bccb_substreams_for(bccb_plan_t plan, int batch);
+
 /* Kernel path: 0 = automatic (small-grid persistent solver, shape-specialised and fused
  * kernels, generic fallback), 1 = generic runtime-shape kernels only.  Results agree to
  * floating-point rounding (the paths evaluate the soft threshold with different float64

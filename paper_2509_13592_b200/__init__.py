@@ -5,7 +5,7 @@ Drop-in for the hot path of the reference package `bccblasso`
 the ista/fista/admm solver entry points, batched over snapshots and executed by
 hand-written CUDA through the C ABI in include/bccb_b200.h.
 
-Importing the package requires the built shared library (no CPU fallback);
+The first GPU call requires the built shared library (no CPU fallback);
 build it with `python paper_2509_13592_b200/_build.py`.
 """
 

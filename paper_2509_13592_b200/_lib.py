@@ -1,8 +1,12 @@
 """ctypes binding of the C ABI declared in include/bccb_b200.h.
 
-The product path has no CPU fallback: if the shared library is missing this
-module raises at import time, and every call checks the C status code and
-raises the reference's exception class (pkg/src/bccblasso/errors.py:4-65).
+The library is mapped lazily, on the first access to `lib` (PEP 562 module
+`__getattr__`), so host-only modules of the package (scenes, arrays, errors,
+textio) import without mapping the CUDA library: the CPU reference arm of
+bench.py and the oracle workers stay free of it.  The product path has no CPU
+fallback: the first GPU call raises ImportError if the shared library is
+missing, and every call checks the C status code and raises the reference's
+exception class (pkg/src/bccblasso/errors.py:4-65).
 """
 
 import ctypes
@@ -50,6 +54,7 @@ SIGNATURES = {
     "bccb_profile_begin": (_i, []),
     "bccb_profile_end": (_i, [_vp, _vp]),
     "bccb_set_substreams": (_i, [_i]),
+    "bccb_substreams_for": (_i, [_vp, _i]),
     "bccb_set_path": (_i, [_i]),
 }
 
@@ -68,7 +73,21 @@ def _load():
     return lib
 
 
-lib = _load()
+_loaded = None
+
+
+def __getattr__(name):
+    global _loaded
+    if name == "lib":
+        if _loaded is None:
+            _loaded = _load()
+        return _loaded
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+
+
+def is_loaded() -> bool:
+    """True once the CUDA library has been mapped into this process."""
+    return _loaded is not None
 
 
 class CudaError(BccbLassoError, RuntimeError):
@@ -80,7 +99,7 @@ class UnsupportedSizeError(InvalidArgumentError):
 
 
 def last_error() -> str:
-    return lib.bccb_last_error().decode(errors="replace")
+    return __getattr__("lib").bccb_last_error().decode(errors="replace")
 
 
 def check(status: int, iteration: int | None = None) -> None:

@@ -87,6 +87,14 @@ static void prof_after(ProfEvent* e, cudaStream_t st) {
 
 extern "C" long long bccb_launch_count(void) { return g_launches.load(); }
 
+// Set at the top of every public entry point that launches kernels (EntryScope); consumed by
+// the first launch_pass of the call.
+static thread_local bool t_entry_fresh = false;
+struct EntryScope {
+  EntryScope() { t_entry_fresh = true; }
+  ~EntryScope() { t_entry_fresh = false; }
+};
+
 extern "C" int bccb_profile_begin(void) {
   g_prof_on = true;
   g_prof_used = 0;
@@ -628,7 +636,13 @@ static int launch_pass(KernelT k, int kind, unsigned grid, const LaunchShape& sh
   if (rc) return rc;
   ProfEvent* pe;
   prof_before(kind, st, &pe);
-  if (pdl_mode() > 0) {
+  // The first kernel of a public entry point follows work this library did not launch (or an
+  // earlier call whose kernels may release dependents before their last stores): it is
+  // launched without the programmatic-serialization attribute, so every read it makes, even
+  // one placed before its griddepcontrol.wait, sees the finished predecessor.
+  const bool entry_first = t_entry_fresh;
+  t_entry_fresh = false;
+  if (pdl_mode() > 0 && !entry_first) {
     // programmatic dependent launch: every kernel of bccb_kernels.cuh starts with pdl_wait()
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1114,16 +1128,19 @@ static int matvec_impl(bccb_plan_t p, int batch, const void* x, void* y, void* w
 
 extern "C" int bccb_matvec(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
                            void* stream) {
+  EntryScope entry_scope_;
   return matvec_impl<float2>(p, batch, x, y, workspace, stream);
 }
 
 extern "C" int bccb_matvec_z(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
                              void* stream) {
+  EntryScope entry_scope_;
   return matvec_impl<double2>(p, batch, x, y, workspace, stream);
 }
 
 extern "C" int bccb_spectrum_box(bccb_plan_t p, int batch, const void* x, void* out_box,
                                  void* workspace, void* stream) {
+  EntryScope entry_scope_;
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!x || !out_box) return fail(BCCB_ERR_INVALID, "x / out_box is NULL");
@@ -1138,6 +1155,7 @@ extern "C" int bccb_spectrum_box(bccb_plan_t p, int batch, const void* x, void* 
 extern "C" int bccb_synthesize(bccb_plan_t p, int batch, const void* box, float scale, const void* x,
                                float alpha, void* out, float* maxabs, void* workspace,
                                void* stream) {
+  EntryScope entry_scope_;
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!box) return fail(BCCB_ERR_INVALID, "box is NULL");
@@ -1174,6 +1192,7 @@ __global__ void adjoint_scatter_kernel(const float2* __restrict__ y, const int* 
 
 extern "C" int bccb_adjoint(bccb_plan_t p, int batch, const void* y, void* bhat_box, void* b,
                             float* maxabs, void* workspace, void* stream) {
+  EntryScope entry_scope_;
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!p->occ_dev || p->M < 1) return fail(BCCB_ERR_INVALID, "bccb_adjoint needs a Gram plan");
@@ -1259,8 +1278,18 @@ static int sub_batches(const bccb_plan_s* p, int batch) {
                           // with the warp column pass 2: 202.1, 3: 202.5, 4: 196.5, 5: 179.4)
   }
   n = std::max(1, std::min(n, bccb_plan_s::MAX_SUB));
-  while (n > 1 && (batch < n || (long long)(batch / n) * p->L2 < 2048)) --n;
+  // BCCB_SUB_MIN_LINES lowers the per-part floor so small test batches exercise the split
+  static const long long min_lines = [] {
+    const char* e = getenv("BCCB_SUB_MIN_LINES");
+    return e ? std::max(1LL, atoll(e)) : 2048LL;
+  }();
+  while (n > 1 && (batch < n || (long long)(batch / n) * p->L2 < min_lines)) --n;
   return n;
+}
+
+extern "C" int bccb_substreams_for(bccb_plan_t p, int batch) {
+  if (!p || batch < 1) return 1;
+  return sub_batches(p, batch);
 }
 
 static int ensure_aux_streams(bccb_plan_s* p, int n) {
@@ -1397,6 +1426,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
                               double mu, const double* tau,
                               const void* bhat_box, const void* extra, void* c, void* d,
                               int* first_bad, void* workspace, void* stream) {
+  EntryScope entry_scope_;
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (iterations < 1) return fail(BCCB_ERR_INVALID, "iteration count must be positive");
@@ -1719,6 +1749,7 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
                              double rho, const double* tau,
                              const void* bhat_box, const void* extra, void* z, void* v, void* c_last,
                              int* first_bad, void* workspace, void* stream) {
+  EntryScope entry_scope_;
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (iterations < 1) return fail(BCCB_ERR_INVALID, "iteration count must be positive");
@@ -1776,6 +1807,7 @@ extern "C" size_t bccb_topk_workspace_bytes(int batch, long long length, int k) 
 
 extern "C" int bccb_topk(int batch, long long length, const void* values, int is_double, int k,
                          int* idx, float* mag, void* workspace, void* stream) {
+  EntryScope entry_scope_;
   if (batch < 1 || length < 1) return fail(BCCB_ERR_INVALID, "empty input");
   if (k < 1 || k > 64) return fail(BCCB_ERR_INVALID, "k must lie in [1, 64]");
   if (k > length) return fail(BCCB_ERR_INVALID, "k exceeds the vector length");

@@ -3,7 +3,9 @@
 Snapshots are independent (same geometry, Lambda and mu; per-snapshot tau), so
 rank r solves the contiguous slice [r*B/P, (r+1)*B/P) and the only collective is
 one gather to rank 0 after the loop: recovered spectra and peak
-lists, over NCCL (NVLink/NVSwitch) on GPUs or gloo in the CPU tests.
+lists, as grouped point-to-point sends into rank 0's output (NCCL over
+NVLink/NVSwitch on GPUs, gloo in the CPU tests).  This replaces the reference's
+sequential per-trial sweep (pkg/src/bccblasso/experiments.py:330-349).
 """
 
 import os
@@ -45,32 +47,59 @@ def init(backend: str | None = None) -> tuple[int, int, int]:
     return rank, world, local
 
 
-def gather_rows(local: torch.Tensor, total_rows: int, root: int = 0):
-    """Gather row-sharded tensors (dim 0 split by shard_bounds) to `root`.
+def workload_shard(batch: int, rank: int, world: int, strong: bool) -> tuple[int, int]:
+    """Snapshot slice [lo, hi) this rank solves.
 
-    Returns the (total_rows, ...) tensor on root and None elsewhere.  Uneven shards
-    are padded to the largest shard for the single all-gather-into-tensor call.
+    strong=True : the global batch `batch` is split over the ranks (BASELINE configs 4/5:
+                  "batch 1024 / 32 sharded across 1/2/4/8 GPUs"; SURVEY 8(e));
+    strong=False: every rank solves its own `batch` snapshots (weak scaling).
+    """
+    if strong:
+        return shard_bounds(batch, rank, world)
+    return rank * batch, (rank + 1) * batch
+
+
+def _flat(t: torch.Tensor) -> torch.Tensor:
+    # NCCL moves real dtypes; complex rows travel as interleaved (re, im) pairs
+    return torch.view_as_real(t) if t.is_complex() else t
+
+
+def gather_rows(local: torch.Tensor, total_rows: int, root: int = 0, out: torch.Tensor | None = None):
+    """Gather row-sharded tensors (dim 0 split by shard_bounds) to `root` only.
+
+    One grouped point-to-point exchange (NCCL send/recv over NVLink, or gloo on CPU):
+    every other rank sends its rows straight into its slice of root's (total_rows, ...)
+    output, so nothing is padded, concatenated or received by the non-root ranks
+    (the only collective of the path).  Returns the full tensor on root
+    (`out` if given) and None elsewhere.
     """
     if not dist.is_initialized() or dist.get_world_size() == 1:
-        return local
+        if out is None:
+            return local
+        out.copy_(local)
+        return out
     world, rank = dist.get_world_size(), dist.get_rank()
-    biggest = max(shard_bounds(total_rows, r, world)[1] - shard_bounds(total_rows, r, world)[0]
-                  for r in range(world))
-    pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
-    if local.is_complex():
-        pad = torch.view_as_real(pad)
-    flat = torch.empty((world * pad.shape[0],) + tuple(pad.shape[1:]), dtype=pad.dtype, device=pad.device)
-    dist.all_gather_into_tensor(flat, pad)
-    out = flat.view((world,) + tuple(pad.shape))
+    bounds = [shard_bounds(total_rows, r, world) for r in range(world)]
+    lo, hi = bounds[rank]
+    if local.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} holds {local.shape[0]} rows, its shard is {hi - lo}")
     if rank != root:
+        if hi > lo:
+            for req in dist.batch_isend_irecv([dist.P2POp(dist.isend, _flat(local.contiguous()), root)]):
+                req.wait()
         return None
-    parts = []
-    for r in range(world):
-        lo, hi = shard_bounds(total_rows, r, world)
-        parts.append(out[r, : hi - lo])
-    full = torch.cat(parts, dim=0)
-    return torch.view_as_complex(full.contiguous()) if local.is_complex() else full
+    if out is None:
+        out = torch.empty((total_rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    ops = []
+    for r, (a, b) in enumerate(bounds):
+        if r == root:
+            out[a:b].copy_(local)
+        elif b > a:
+            ops.append(dist.P2POp(dist.irecv, _flat(out[a:b]), r))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
 
 
 def max_over_ranks(value: float) -> float:

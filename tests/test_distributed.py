@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2509_13592_b200.distributed import gather_rows, max_over_ranks, shard_bounds
+from paper_2509_13592_b200.distributed import gather_rows, max_over_ranks, shard_bounds, workload_shard
 
 
 def test_shard_bounds_partition():
@@ -58,12 +58,20 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         total = 7
-        lo, hi = shard_bounds(total, rank, world)
+        # bench.py's own shard choice (strong scaling of a fixed global batch, configs 4/5)
+        lo, hi = workload_shard(total, rank, world, strong=True)
         local = torch.from_numpy(_solve_shard(lo, hi))
-        full = gather_rows(local, total)
+        # bench.py's e2e gather: spectra (complex) and peak lists (int32) into rank 0's output only
+        out = torch.empty((total, local.shape[1]), dtype=local.dtype) if rank == 0 else None
+        full = gather_rows(local, total, out=out)
+        idx = torch.arange(lo * 3, hi * 3, dtype=torch.int32).reshape(hi - lo, 3)
+        idx_full = gather_rows(idx, total)
         m = max_over_ranks(float(rank + 1))
         if rank == 0:
-            q.put((full.numpy(), m))
+            assert full is out
+            q.put((full.numpy(), idx_full.numpy(), m))
+        else:
+            assert full is None and idx_full is None
     finally:
         dist.destroy_process_group()
 
@@ -75,9 +83,17 @@ def test_gloo_two_rank_gather_matches_single_process():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    full, m = q.get(timeout=120)
+    full, idx, m = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     np.testing.assert_array_equal(full, _solve_shard(0, 7))
+    np.testing.assert_array_equal(idx, np.arange(21, dtype=np.int32).reshape(7, 3))
     assert m == 2.0
+
+
+def test_workload_shard_strong_and_weak():
+    # strong: BASELINE configs 4/5 split the fixed global batch; weak: every rank its own batch
+    assert [workload_shard(32, r, 8, True) for r in range(8)] == [(4 * r, 4 * r + 4) for r in range(8)]
+    assert [workload_shard(1024, r, 3, True) for r in range(3)] == [(0, 342), (342, 683), (683, 1024)]
+    assert [workload_shard(64, r, 2, False) for r in range(2)] == [(0, 64), (64, 128)]

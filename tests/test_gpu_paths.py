@@ -177,10 +177,15 @@ def test_substream_split_is_bitwise_neutral(substreams):
     """The sub-batch split runs independent snapshots on up to 8 streams (with programmatic
     dependent launch between the passes of each stream): FISTA (config 2 shape) and the split
     ADMM (config 3 shape, small threshold so z leaves zero) give identical bits for every split."""
-    w, geom, op, bs, taus = scene_problem(2, 16)
+    w, geom, op, bs, taus = scene_problem(2, 64)
     mu = 1.0 / (w.l1 * w.l2)
     conf = bb.SolverConfig(iterations=60, step_size_mu=mu)
-    outs = [substreams(n, lambda: bb.fista_solve(bb.LassoProblem(op, bs, taus), conf).estimate) for n in (1, 3, 8)]
+    # 64 config-2 snapshots: 3, 4 and 8 parts keep >= 2048 lines each, so each split really runs
+    from paper_2509_13592_b200 import _lib as lib_
+    for n in (3, 4, 8):
+        assert substreams(n, lambda: lib_.lib.bccb_substreams_for(op._plan, 64)) == n
+    outs = [substreams(n, lambda: bb.fista_solve(bb.LassoProblem(op, bs, taus), conf).estimate)
+            for n in (1, 3, 4, 8)]
     for o in outs[1:]:
         np.testing.assert_array_equal(o, outs[0])
     w3 = scenes.workload(3)
@@ -243,7 +248,7 @@ def test_launch_modes_agree(tmp_path, env, bitwise):
     outs = []
     for extra in ({}, env):
         out = tmp_path / f"est{len(outs)}.npy"
-        e = dict(os.environ, **extra)
+        e = dict(os.environ, BCCB_SUB_MIN_LINES="256", **extra)
         subprocess.run([sys.executable, str(script), root, str(out), "2"], check=True, env=e, timeout=600)
         outs.append(np.load(out))
     if bitwise:
@@ -253,7 +258,7 @@ def test_launch_modes_agree(tmp_path, env, bitwise):
             assert orc.rel_l2(a, b) < 1e-6
 
 
-@pytest.mark.parametrize("pdl", ["1", "0"])
+@pytest.mark.parametrize("pdl", ["1", "2"])
 def test_fused_column_pass_pdl(tmp_path, pdl):
     """The fused column pass (rows kernel whose last CTA per snapshot runs the column pass; taken
     at L1 = 64 when the cluster and small-grid solvers are off) has no separate column pass
@@ -301,7 +306,7 @@ def test_pdl_bitwise_across_solvers(tmp_path, cfg, solver, iters):
     outs = []
     for extra in ({"BCCB_PDL": "1"}, {}, {"BCCB_PDL": "0"}):
         out = tmp_path / f"est{len(outs)}.npy"
-        e = dict(os.environ, **extra)
+        e = dict(os.environ, BCCB_SUB_MIN_LINES="256", **extra)
         subprocess.run([sys.executable, str(script), root, str(out), str(cfg), solver, str(iters)], check=True, env=e,
                        timeout=600)
         outs.append(np.load(out))

@@ -136,3 +136,22 @@ def test_separated_targets_config5():
             d1 = abs(t[i].f1 - t[j].f1) % 1.0
             d2 = abs(t[i].f2 - t[j].f2) % 1.0
             assert min(d1, 1 - d1) >= 1 / w.l1 or min(d2, 1 - d2) >= 1 / w.l2
+
+
+def test_host_modules_do_not_map_the_cuda_library():
+    """The CPU reference arm of bench.py and the oracle workers import the package's host
+    modules (scenes, arrays) but must not map libbccb_b200.so (the library loads lazily on
+    the first GPU call)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, sys.argv[1]);"
+            "import paper_2509_13592_b200, paper_2509_13592_b200.scenes, oracle.bccb_oracle;"
+            "from paper_2509_13592_b200 import _lib;"
+            "maps = open('/proc/self/maps').read();"
+            "assert 'libbccb_b200' not in maps and not _lib.is_loaded(), 'library mapped at import';"
+            "_lib.lib;"
+            "assert 'libbccb_b200' in open('/proc/self/maps').read() and _lib.is_loaded();"
+            "print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
