@@ -129,6 +129,19 @@ int bccb_fista_run(bccb_plan_t plan, int batch, int first_iteration, int iterati
                    const void* bhat_box, const void* extra, void* c, void* d, int* first_bad,
                    void* workspace, void* stream);
 
+/* bccb_fista_run from iteration 0 with the objective trace of solvers.py:233-242,
+ * f(c_{t+1}) - ||y||^2 = -2 Re<b, c> + Re<c, G c> + tau ||c||_1, accumulated on the device for
+ * every iteration inside the same pass kernels (record_objective=True without a host round
+ * trip; replaces the trace lines solvers.py:272-280 and 340-343).  The quadratic part is taken
+ * on the spectral box by Parseval; tau ||c||_1 is summed by the rows pass.
+ *   trace : device double [batch][iterations] <- the objective minus ||y||^2 (caller adds it)
+ * Returns BCCB_ERR_UNSUPPORTED (the caller falls back to per-iteration reductions) unless the
+ * plan is a Gram-type operator (zero spectrum outside the box), b lies on the box (no extra)
+ * and the grid has a specialised rows pass. */
+int bccb_fista_run_traced(bccb_plan_t plan, int batch, int iterations, double mu, const double* tau,
+                          const void* bhat_box, void* c, void* d, int* first_bad, double* trace,
+                          void* workspace, void* stream);
+
 /* ADMM: iterations first_iteration .. first_iteration+iterations-1, fused and in place.
  * Replaces admm_solve (solvers.py:385-448): precompute P = (G + rho I)^-1, q = P b
  * (403-415) folded into the spectral box; loop c = q + rho P(z - v), z = S_{rho tau}(c + v),

@@ -14,7 +14,11 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libbccb_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 SOURCES = ["bccb_capi.cu"]
-HEADERS = ["band_fft.cuh", "bccb_kernels.cuh", "topk.cuh"]
+HEADERS = ["band_fft.cuh", "bccb_kernels.cuh", "topk.cuh", "tcgen05.cuh"]
+# self-test of the tcgen05 primitives (tests/test_gpu_tc.py only; not on any product path)
+PROBE_NAME = "libbccb_tcprobe.so"
+PROBE_PATH = os.path.join(PKG_DIR, PROBE_NAME)
+PROBE_SOURCES = ["tc_probe.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -31,26 +35,32 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build the sm_100a library")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB_PATH):
+def _stale(path, sources) -> bool:
+    if not os.path.exists(path):
         return True
-    lib_mtime = os.path.getmtime(LIB_PATH)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    lib_mtime = os.path.getmtime(path)
+    deps = [os.path.join(CSRC, f) for f in sources + HEADERS]
     deps.append(os.path.join(PKG_DIR, "..", "include", "bccb_b200.h"))
     return any(os.path.getmtime(d) > lib_mtime for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/*.cu into LIB_PATH when sources are newer; return the library path."""
-    if not force and not _stale():
-        return LIB_PATH
-    tmp = LIB_PATH + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+def _compile(path, sources, verbose):
+    tmp = path + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp] + [os.path.join(CSRC, s) for s in sources]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, path)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into LIB_PATH (and the tcgen05 self-test library) when sources are
+    newer; return the library path."""
+    if force or _stale(PROBE_PATH, PROBE_SOURCES):
+        _compile(PROBE_PATH, PROBE_SOURCES, verbose)
+    if force or _stale(LIB_PATH, SOURCES):
+        _compile(LIB_PATH, SOURCES, verbose)
     return LIB_PATH
 
 

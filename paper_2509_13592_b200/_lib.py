@@ -47,6 +47,7 @@ SIGNATURES = {
     "bccb_synthesize": (_i, [_vp, _i, _vp, _f, _vp, _f, _vp, _vp, _vp, _vp]),
     "bccb_adjoint": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bccb_fista_run": (_i, [_vp, _i, _i, _i, _d] + [_vp] * 8),
+    "bccb_fista_run_traced": (_i, [_vp, _i, _i, _d] + [_vp] * 8),
     "bccb_admm_run": (_i, [_vp, _i, _i, _i, _d] + [_vp] * 9),
     "bccb_topk_workspace_bytes": (_sz, [_i, _ll, _i]),
     "bccb_topk": (_i, [_i, _ll, _vp, _i, _i, _vp, _vp, _vp, _vp]),

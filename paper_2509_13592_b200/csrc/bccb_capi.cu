@@ -171,6 +171,9 @@ struct AxisHost {
   // (KP <= 16: the KP16 rows engine and the column pass) and its KP <= 8 variant (column
   // passes with few lines: twice the threads per line, shorter latency chains)
   AxisPrec f, d, s, s8;
+  // tensor-core rows engine (rows axis only): R = 128 threads per line, KP = N / 128,
+  // Mo = K / KP a multiple of 4 (KP = 0: not eligible)
+  AxisPrec t;
   template <typename C>
   const AxisPrec& prec() const;
   template <typename C>
@@ -185,6 +188,18 @@ struct AxisHost {
     a.pitch = p.pitch;
     a.tw1 = (const C*)p.tw1;
     a.tw2 = (const C*)p.tw2;
+    return a;
+  }
+  AxisT<float2> dev_t() const {
+    AxisT<float2> a;
+    a.N = N;
+    a.K = K;
+    a.KP = t.KP;
+    a.R = t.R;
+    a.Mo = t.Mo;
+    a.pitch = t.pitch;
+    a.tw1 = (const float2*)t.tw1;
+    a.tw2 = (const float2*)t.tw2;
     return a;
   }
   AxisT<float2> dev_s(bool narrow = false) const {
@@ -288,11 +303,23 @@ static int make_axis(int N, int Kreq, AxisHost& ax, bool cols) {
   if (!rc) rc = upload_twiddles<double2>(N, ax.d);
   if (!rc) rc = upload_twiddles<float2>(N, ax.s);
   if (!rc) rc = upload_twiddles<float2>(N, ax.s8);
+  ax.t = AxisPrec{};
+  ax.t.KP = 0;
+  if (!rc && !cols && N % 128 == 0) {
+    const int kp = N / 128;
+    if ((kp == 8 || kp == 16 || kp == 32) && K % kp == 0 && (K / kp) % 4 == 0 && K / kp <= 16) {
+      ax.t.KP = kp;
+      ax.t.R = 128;
+      ax.t.Mo = K / kp;
+      ax.t.pitch = 129;
+      rc = upload_twiddles<float2>(N, ax.t);
+    }
+  }
   return rc;
 }
 
 static void free_axis(AxisHost& a) {
-  for (AxisPrec* p : {&a.f, &a.d, &a.s, &a.s8}) {
+  for (AxisPrec* p : {&a.f, &a.d, &a.s, &a.s8, &a.t}) {
     cudaFree(p->tw1);
     cudaFree(p->tw2);
   }
@@ -499,11 +526,40 @@ static bool kp16_shape(const AxisPrec& a) {
   return a.KP == 16 && ((a.R == 16 && a.Mo == 2) || (a.R == 64 && a.Mo == 4));
 }
 static bool rows_use_kp16(const AxisHost& ax) { return rows_kp16_env() && kp16_shape(ax.s); }
-static const AxisPrec& rows_axis(const AxisHost& ax) { return rows_use_kp16(ax) ? ax.s : ax.f; }
+
+// Tensor-core rows engine of the specialised FISTA/ISTA pass (BCCB_ROWS_TC, default on): the
+// level-2 stage of the band inverse runs as tcgen05 kind::tf32 MMAs (bccb_kernels.cuh TcInv).
+// Shapes with an instantiation: (KP, Mo) at R = 128.
+#define TC_SHAPES(X)                                       \
+  X(32, 4)   /* L1 = 4096, band 128 (config 5) */          \
+  X(8, 8)    /* L1 = 1024, band 64  (config 4) */          \
+  X(16, 4)   /* L1 = 2048, band 64 */                      \
+  X(16, 8)   /* L1 = 2048, band 128 */
+static int rows_tc_env() {
+  static const int v = [] {
+    const char* e = getenv("BCCB_ROWS_TC");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+static bool tc_shape(const AxisPrec& a) {
+  if (a.KP == 0 || a.R != 128) return false;
+#define TC_KEY(KP_, MO_) \
+  if (a.KP == KP_ && a.Mo == MO_) return true;
+  TC_SHAPES(TC_KEY)
+#undef TC_KEY
+  return false;
+}
+static bool rows_use_tc(const AxisHost& ax) { return rows_tc_env() && tc_shape(ax.t); }
+
+// rows engine of the specialised passes: tc = the FISTA/ISTA tensor-core engine
+static const AxisPrec& rows_axis(const AxisHost& ax, bool tc = false) {
+  return tc ? ax.t : (rows_use_kp16(ax) ? ax.s : ax.f);
+}
 
 // threads per CTA of the specialised FISTA rows pass (flags: one 32-bit word per warp)
-static int zs_threads(const AxisHost& ax) { return std::max(256, rows_axis(ax).R); }
-static size_t zs_flag_bytes(const bccb_plan_s* p, int batch);
+static int zs_threads(const AxisHost& ax, bool tc = false) { return std::max(256, rows_axis(ax, tc).R); }
+static size_t zs_flag_bytes(const bccb_plan_s* p, int batch, bool tc = false);
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -517,18 +573,24 @@ static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R, int extra_w
 
 // flags of the specialised FISTA rows pass (complex64 axis): per tile, one word per warp and
 // one tile word (rows_tile)
-static size_t zs_flag_bytes(const bccb_plan_s* p, int batch) {
-  return flag_bytes_for(p, batch, rows_axis(p->ax1).R, 1);
-}
-
 // flags of the specialised ADMM rows pass (complex128 axis)
 static size_t zs_flag_bytes_d(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, p->ax1.d.R); }
+
+static size_t zs_flag_bytes(const bccb_plan_s* p, int batch, bool tc) {
+  return flag_bytes_for(p, batch, rows_axis(p->ax1, tc).R, 1);
+}
+static size_t zs_flag_bytes_max(const bccb_plan_s* p, int batch) {
+  size_t b = std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch));
+  if (p->ax1.t.KP > 0) b = std::max(b, zs_flag_bytes(p, batch, true));
+  return b;
+}
+
 
 static size_t ws_bytes(const bccb_plan_s* p, int batch) {
   const size_t inter = (size_t)batch * p->ax1.K * p->L2 * sizeof(double2);
   const size_t box = (size_t)p->ax1.K * p->ax2.K * sizeof(double2);
   return 2 * align_up(inter) + 2 * align_up(box) +
-         align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch))) +
+         align_up(zs_flag_bytes_max(p, batch)) +
          align_up((size_t)batch * sizeof(int)) + 2 * align_up((size_t)batch * box);
 }
 
@@ -546,7 +608,7 @@ static Workspace carve(const bccb_plan_s* p, int batch, void* base) {
   w.P = ptr;
   ptr += box;
   w.flags = (unsigned char*)ptr;
-  ptr += align_up(std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch)));
+  ptr += align_up(zs_flag_bytes_max(p, batch));
   w.counters = (int*)ptr;
   ptr += align_up((size_t)batch * sizeof(int));
   w.vs = ptr;
@@ -816,6 +878,57 @@ static FusedCols make_fused(const bccb_plan_s* p, int batch, const Workspace& w,
   return fc;
 }
 
+// Tensor-core rows pass (rows_fista_tc_kernel): persistent CTAs (resident CTAs per SM x SMs),
+// shared memory = band tile + forward transpose + staged twiddles + A tiles + B tiles.
+template <int KP, int MO, bool MOM>
+static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
+                           const EpiFista& epi, unsigned* fl, cudaStream_t st) {
+  using TS = TileShape<KP, 128, MO>;
+  using TSH = TcShape<KP, MO, TS::TR>;
+  // resident CTAs per SM the register budget targets: the KP-point register DFT dominates
+  constexpr int MINB = KP == 8 ? 4 : (KP == 16 ? 3 : 2);
+  auto k = rows_fista_tc_kernel<KP, MO, MOM, MINB>;
+  size_t smem = (size_t)(TS::TR * TS::XP + TS::TR * TS::SP) * sizeof(float2);
+  if (TS::STAGE_TW) smem += (size_t)(KP + MO) * 128 * sizeof(float2);
+  smem = ((smem + 127) & ~(size_t)127) + TSH::A_BYTES + TSH::B_BYTES;
+  static int occ[2] = {0, 0};            // per MOM instantiation: resident CTAs per SM
+  int& o = occ[MOM ? 1 : 0];
+  if (!o) {
+    int rc = prep_smem(k, smem);
+    if (rc) return rc;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 256, smem));
+    if (o < 1) return fail(BCCB_ERR_UNSUPPORTED, "tensor-core rows pass does not fit one SM");
+    // every resident CTA holds TSH::COLS TMEM columns (512 per SM)
+    if (o * TSH::COLS > 512) o = 512 / TSH::COLS;
+  }
+  const int ntiles = (int)((G.rows + TS::TR - 1) / TS::TR);
+  const unsigned grid = (unsigned)std::min<long long>(ntiles, (long long)o * num_sms());
+  LaunchShape sh;
+  sh.threads = 256;
+  sh.TR = TS::TR;
+  sh.smem = smem;
+  return launch_pass<float2>(k, KIND_ROWS, grid, sh, st, G, ax, io, epi, fl, ntiles);
+}
+
+static int launch_rows_fista_tc(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
+                                const EpiFista& epi, cudaStream_t st) {
+  LaunchShape sh;
+  sh.threads = 256;
+  sh.TR = 2;
+  const Geo G = rows_geo(p, batch, sh, inv, fwd);
+  RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
+  const AxisT<float2> ax = p->ax1.dev_t();
+  unsigned* fl = (unsigned*)w.flags;
+  const bool mom = epi.momentum != 0;
+#define TC_CASE(KP_, MO_)                                                                \
+  if (ax.KP == KP_ && ax.Mo == MO_)                                                      \
+    return mom ? launch_tc_shape<KP_, MO_, true>(p, G, ax, io, epi, fl, st)              \
+               : launch_tc_shape<KP_, MO_, false>(p, G, ax, io, epi, fl, st);
+  TC_SHAPES(TC_CASE)
+#undef TC_CASE
+  return fail(BCCB_ERR_UNSUPPORTED, "no tensor-core rows specialisation (KP %d, Mo %d)", ax.KP, ax.Mo);
+}
+
 static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                                   const EpiFista& epi, bool zs, cudaStream_t st, const FusedCols* fused = nullptr) {
   LaunchShape sh = fast_shape(p);
@@ -940,12 +1053,23 @@ static int launch_zero_segments_z(const bccb_plan_s* p, int batch, const Workspa
 
 template <typename T2>
 static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace& w, double2* c, T2* d,
-                                cudaStream_t st) {
+                                cudaStream_t st, bool tc = false) {
   LaunchShape sh = fast_shape(p);
+  if (tc) {
+    sh.threads = 256;
+    sh.TR = 2;
+  }
   const Geo G = rows_geo(p, batch, sh, false, false);
   sh.smem = 0;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   const unsigned* fl = (const unsigned*)w.flags;
+  if (tc) {
+    const int kp = p->ax1.t.KP;
+    if (kp == 8) return launch_pass<float2>(zero_segments_kernel<8, 128, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (kp == 16) return launch_pass<float2>(zero_segments_kernel<16, 128, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (kp == 32) return launch_pass<float2>(zero_segments_kernel<32, 128, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    return fail(BCCB_ERR_UNSUPPORTED, "no tensor-core zero-segment specialisation");
+  }
   if (rows_use_kp16(p->ax1)) {
     if (p->ax1.s.R == 16) return launch_pass<float2>(zero_segments_kernel<16, 16, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
     if (p->ax1.s.R == 64) return launch_pass<float2>(zero_segments_kernel<16, 64, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
@@ -1026,7 +1150,8 @@ static int launch_cols_warp(const bccb_plan_s* p, const AxisPrec& a, const Geo& 
 
 template <typename C>
 static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, const Workspace& w,
-                       const C* D, const C* P, const float2* Bh, C* box_out, cudaStream_t st) {
+                       const C* D, const C* P, const float2* Bh, C* box_out, cudaStream_t st,
+                       const ObjBox* ob = nullptr) {
   const bool stream_axis = std::is_same<C, float2>::value;
   const bool narrow = stream_axis && cols_narrow(p, batch);
   const LaunchShape sh = stream_axis ? shape_for_prec(p->ax2, narrow ? p->ax2.s8 : p->ax2.s, sizeof(C),
@@ -1039,7 +1164,7 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   G.TR = sh.TR;
   G.do_fwd = fwd ? 1 : 0;
   G.do_inv = inv ? 1 : 0;
-  ColsIO<C> io;
+  ColsIO<C> io{};
   io.U = (const C*)w.U;
   io.V = (C*)w.V;
   io.D = D;
@@ -1047,6 +1172,7 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   io.Bh = Bh;
   io.box_out = box_out;
   io.K1 = p->ax1.K;
+  if (ob) io.ob = *ob;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
   if constexpr (std::is_same<C, float2>::value) {
     const AxisT<C> ax = p->ax2.dev_s(narrow);
@@ -1422,11 +1548,31 @@ static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const E
   return fail(BCCB_ERR_UNSUPPORTED, "no small-grid specialisation");
 }
 
+static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int iterations, double mu,
+                          const double* tau, const void* bhat_box, const void* extra, void* c, void* d,
+                          int* first_bad, void* workspace, void* stream, double* trace);
+
 extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int iterations,
                               double mu, const double* tau,
                               const void* bhat_box, const void* extra, void* c, void* d,
                               int* first_bad, void* workspace, void* stream) {
   EntryScope entry_scope_;
+  return fista_run_impl(p, batch, first_iteration, iterations, mu, tau, bhat_box, extra, c, d, first_bad,
+                        workspace, stream, nullptr);
+}
+
+extern "C" int bccb_fista_run_traced(bccb_plan_t p, int batch, int iterations, double mu, const double* tau,
+                                     const void* bhat_box, void* c, void* d, int* first_bad, double* trace,
+                                     void* workspace, void* stream) {
+  EntryScope entry_scope_;
+  if (!trace) return fail(BCCB_ERR_INVALID, "NULL trace");
+  return fista_run_impl(p, batch, 0, iterations, mu, tau, bhat_box, nullptr, c, d, first_bad, workspace, stream,
+                        trace);
+}
+
+static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int iterations, double mu,
+                          const double* tau, const void* bhat_box, const void* extra, void* c, void* d,
+                          int* first_bad, void* workspace, void* stream, double* trace) {
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (iterations < 1) return fail(BCCB_ERR_INVALID, "iteration count must be positive");
@@ -1449,6 +1595,8 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   e.kscale = mu;
   e.extra_scale = mu;
   e.momentum = d ? 1 : 0;
+  e.trace = nullptr;
+  e.trace_stride = 0;
   // momentum coefficients: beta_t = (alpha_{t-1} - 1) / alpha_t, alpha_0 = 1 (solvers.py:294-337)
   const int t_end = first_iteration + iterations;
   std::vector<double> beta((size_t)t_end + 1, 0.0);
@@ -1460,18 +1608,27 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
       alpha = an;
     }
   }
+  // fused objective trace: the per-pass kernels with zero-segment skipping, a Gram-type
+  // spectrum (zero outside the box) and the right-hand side on the box
+  if (trace) {
+    if (first_iteration != 0 || extra || p->lam_out != std::complex<double>(0.0, 0.0) ||
+        !fast_supported(p, batch, extra))
+      return fail(BCCB_ERR_UNSUPPORTED, "fused objective trace needs a Gram operator on a specialised grid");
+    CUDA_TRY(cudaMemsetAsync(trace, 0, (size_t)batch * iterations * sizeof(double), st));
+  }
   // 64 x 64 grids: one 8-CTA cluster per snapshot runs the whole solve (distributed shared memory)
-  if (cluster_supported(p, extra))
+  if (!trace && cluster_supported(p, extra))
     return launch_cluster64(p, batch, first_iteration, iterations, e, (const float2*)w.D, (const float2*)w.P,
                             (const float2*)bhat_box, st);
   // small grids: the whole solve in one persistent launch per snapshot (shared-memory state)
-  if (small_supported(p, extra, e.momentum != 0))
+  if (!trace && small_supported(p, extra, e.momentum != 0))
     return launch_small(p, batch, first_iteration, iterations, e, (const float2*)w.D, (const float2*)w.P,
                         (const float2*)bhat_box, st);
   // specialised shapes use zero-segment skipping: flags start all-ones (read everything) and
   // the skipped zeros are written back by one final pass
   const bool zs = fast_supported(p, batch, extra);
-  if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes(p, batch), st));
+  const bool tcr = zs && rows_use_tc(p->ax1);   // tensor-core rows engine (its own tiling)
+  if (zs) CUDA_TRY(cudaMemsetAsync(w.flags, 0xff, zs_flag_bytes(p, batch, tcr), st));
 
   // Sub-batch split: two halves of the batch run on two streams, so one half's (latency-bound)
   // column pass and kernel tails overlap the other half's rows pass.  Snapshots are
@@ -1493,7 +1650,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
     const long long inter = (long long)u.b0 * p->ax1.K * p->L2;
     u.w.U = (float2*)w.U + inter;
     u.w.V = (float2*)w.V + inter;
-    if (zs) u.w.flags = w.flags + zs_flag_bytes(p, u.b0);
+    if (zs) u.w.flags = w.flags + zs_flag_bytes(p, u.b0, tcr);
     u.e = e;
     const long long off = (long long)u.b0 * p->L1 * p->L2;
     u.e.c = e.c + off;
@@ -1504,9 +1661,30 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
     u.e.it = first_iteration;
     u.e.beta_cur = u.e.momentum ? beta[first_iteration] : 0.0;
     u.e.beta_next = 0.0;
+    if (trace) {
+      u.e.trace = trace + (long long)u.b0 * iterations;
+      u.e.trace_stride = iterations;
+    }
   }
+  // objective box terms of the column pass of iteration t (X = FFT2(x_t)): C_t from X_t and
+  // C_{t-1} (workspace cb, float64), quadratic part into trace column t - 1
+  auto obj_box = [&](int q, int t) {
+    ObjBox ob{};
+    const Sub& u = sub[q];
+    const long long boxo = (long long)u.b0 * p->ax1.K * p->ax2.K;
+    ob.chat = (double2*)w.cb + boxo;
+    ob.lam = p->lam_box_dev;
+    ob.bh = (const float2*)bhat_box + boxo;
+    ob.trace = t >= 1 ? u.e.trace : nullptr;
+    ob.stride = iterations;
+    ob.col = t - 1;
+    ob.beta = (u.e.momentum && t >= 1) ? beta[t] : 0.0;
+    ob.inv_L = 1.0 / ((double)p->L1 * p->L2);
+    ob.K2 = p->ax2.K;
+    return ob;
+  };
   const float2* bh = (const float2*)bhat_box;
-  const bool fuse = zs && fused_supported(p);
+  const bool fuse = zs && !tcr && !trace && fused_supported(p);
   FusedCols fcs[bccb_plan_s::MAX_SUB];
   for (int q = 0; q < nsub && fuse; ++q)
     fcs[q] = make_fused(p, sub[q].nb, sub[q].w, (const float2*)w.D, (const float2*)w.P,
@@ -1517,6 +1695,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   }
   auto rows = [&](int q, bool inv, bool fwd) {
     Sub& u = sub[q];
+    if (tcr) return launch_rows_fista_tc(p, u.nb, inv, fwd, u.w, u.e, u.st);
     return zs ? launch_rows_fista_fast(p, u.nb, inv, fwd, u.w, u.e, true, u.st, fuse ? &fcs[q] : nullptr)
               : launch_rows_fista(p, u.nb, inv, fwd, u.w, u.e, u.st);
   };
@@ -1529,18 +1708,28 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
   for (int t = first_iteration; t < t_end; ++t) {
     for (int q = 0; q < nsub; ++q) {
       Sub& u = sub[q];
+      const ObjBox ob = trace ? obj_box(q, t) : ObjBox{};
       if (!fuse &&
           (rc = launch_cols<float2>(p, u.nb, true, true, u.w, (const float2*)w.D, (const float2*)w.P,
-                                    bh + (long long)u.b0 * p->ax1.K * p->ax2.K, nullptr, u.st)))
+                                    bh + (long long)u.b0 * p->ax1.K * p->ax2.K, nullptr, u.st,
+                                    trace ? &ob : nullptr)))
         return rc;
       u.e.it = t;
       u.e.beta_cur = u.e.momentum ? beta[t] : 0.0;
       u.e.beta_next = u.e.momentum ? beta[t + 1] : 0.0;
-      if ((rc = rows(q, true, t + 1 < t_end))) return rc;
+      if ((rc = rows(q, true, t + 1 < t_end || trace))) return rc;
     }
   }
+  // objective of the last iterate: forward-only column pass on FFT2(x_{t_end}) (no V output)
+  for (int q = 0; q < nsub && trace; ++q) {
+    Sub& u = sub[q];
+    const ObjBox ob = obj_box(q, t_end);
+    if ((rc = launch_cols<float2>(p, u.nb, true, false, u.w, (const float2*)w.D, (const float2*)w.P,
+                                  bh + (long long)u.b0 * p->ax1.K * p->ax2.K, nullptr, u.st, &ob)))
+      return rc;
+  }
   for (int q = 0; q < nsub; ++q)
-    if (zs && (rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].e.c, sub[q].e.d, sub[q].st))) return rc;
+    if (zs && (rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].e.c, sub[q].e.d, sub[q].st, tcr))) return rc;
   for (int q = 1; q < nsub; ++q) {
     CUDA_TRY(cudaEventRecord(p->ev_join[q - 1], p->aux[q - 1]));
     CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join[q - 1], 0));

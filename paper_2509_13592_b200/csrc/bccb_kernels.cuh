@@ -17,6 +17,7 @@
 #include <type_traits>
 
 #include "band_fft.cuh"
+#include "tcgen05.cuh"
 
 namespace bccb {
 
@@ -91,6 +92,10 @@ struct EpiFista {
   int* first_bad;                  // [B]
   double a, kscale, extra_scale, beta_cur, beta_next;
   int it, momentum;
+  // fused objective trace (record_objective): tau_b ||c_{t+1}||_1 is added to
+  // trace[b * trace_stride + it] by the rows pass (null: off)
+  double* trace;
+  long long trace_stride;
 
   __device__ __forceinline__ float2 load(long long pos, int) const {
     double2 cc = c[pos];
@@ -232,6 +237,56 @@ __device__ __forceinline__ void rows_forward_store(const Geo& G, const AxisT<C>&
   }
 }
 
+// ------------------------------------------------------------------ fused objective trace
+// The reference's objective (solvers.py:233-242)
+//   f(c) = ||y||^2 - 2 Re<b, c> + Re<c, G c> + tau ||c||_1
+// is evaluated for every iterate c_{t+1} without a host round trip.  By Parseval, with
+// C = FFT2(c) (unnormalised) on the spectral box that carries both Lambda and FFT2(b):
+//   -2 Re<b, c> + <c, G c> = (1/L) sum_box ( Lambda |C|^2 - 2 Re(conj(Bhat) C) ).
+// The column pass already forms X = FFT2(x_t) on the box for the FISTA point
+// x_t = c_t + beta_t (c_t - c_{t-1}); linearity gives C_t = (X_t + beta_t C_{t-1}) / (1 + beta_t)
+// (ISTA: beta = 0, C = X), kept in float64 per box value.  tau ||c||_1 is summed by the rows
+// pass over the points its exact float64 update touched (every other point is exactly zero).
+struct ObjBox {
+  double2* chat;            // [B][K1][K2] C_{t-1} in, C_t out (null: off)
+  const double2* lam;       // [K1][K2] eigenvalues on the box (real for a Gram operator)
+  const float2* bh;         // [B][K1][K2] FFT2(b) on the box
+  double* trace;            // [B][stride]: column `col` receives the quadratic part (null: store only)
+  long long stride;
+  double beta, inv_L;
+  int col, K2;
+};
+
+// quadratic part contributed by band value o of column line `line` (= b K1 + k1)
+__device__ __forceinline__ double obj_term(const ObjBox& ob, long long line, int o, int K1, float2 x) {
+  const long long bi = line * ob.K2 + o;
+  double cr = x.x, ci = x.y;
+  if (ob.beta != 0.0) {
+    const double2 prev = ob.chat[bi];
+    const double inv = 1.0 / (1.0 + ob.beta);
+    cr = (cr + ob.beta * prev.x) * inv;
+    ci = (ci + ob.beta * prev.y) * inv;
+  }
+  ob.chat[bi] = make_double2(cr, ci);
+  if (!ob.trace) return 0.0;
+  const double lam = __ldg(&ob.lam[(line % K1) * ob.K2 + o].x);
+  const float2 bh = ob.bh[bi];
+  return ob.inv_L * (lam * (cr * cr + ci * ci) - 2.0 * ((double)bh.x * cr + (double)bh.y * ci));
+}
+
+// sum v over the lanes of the warp that share key `b` and add it to dst[b * stride] once per
+// group (every lane of the warp calls this; b < 0: no contribution)
+__device__ __forceinline__ void warp_group_add(double* dst, long long stride, long long b, double v) {
+  const unsigned grp = __match_any_sync(0xffffffffu, b);
+  if (grp == 0xffffffffu) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && b >= 0) atomicAdd(dst + b * stride, v);
+  } else if (b >= 0 && v != 0.0) {
+    atomicAdd(dst + b * stride, v);
+  }
+}
+
 // ------------------------------------------------------------------ pass B
 template <typename C>
 struct ColsIO {
@@ -240,8 +295,9 @@ struct ColsIO {
   const C* __restrict__ D;          // [K1][K2] multiplier (null => identity)
   const C* __restrict__ P;          // [K1][K2] rhs multiplier (null => 1)
   const float2* __restrict__ Bh;    // [B][K1][K2] rhs box, complex64 data (null => none)
-  C* __restrict__ box_out;          // [B][K1][K2] (used when !do_inv)
+  C* __restrict__ box_out;          // [B][K1][K2] (used when !do_inv; may be null)
   int K1;
+  ObjBox ob;                        // fused objective trace (ob.chat null: off; complex64 only)
 };
 
 // Default band stage of the column pass: Y = D*X + P*Bh from ColsIO.
@@ -306,26 +362,35 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     }
     __syncthreads();
   }
-  // band values: Y = D*X + P*Bh
+  // band values: Y = D*X + P*Bh   (+ the objective's box terms of X when io.ob.chat is set)
+  constexpr bool OBJ = std::is_same<C, float2>::value && std::is_same<Op, BandMulAdd>::value;
+  long long ob_b = -1;       // snapshot of the running objective sum
+  double ob_v = 0.0;
   for (int idx = tid; idx < TR * K; idx += blockDim.x) {
     const int i2 = idx / K, o = idx - i2 * K;
     const long long g2 = row0 + i2;
     if (g2 >= G.rows) continue;
     C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
     if constexpr (std::is_same<Op, BandMulAdd>::value) {
-      if (pre.ok && idx == tid) {
-        if (G.do_fwd) {
-          y = band_fwd_output(S + i2 * SP, o, KP, ax);
-          if (io.D) y = cmul(y, pre.d);
+      if (G.do_fwd) y = band_fwd_output(S + i2 * SP, o, KP, ax);
+      if constexpr (OBJ) {
+        if (G.do_fwd && io.ob.chat) {
+          const long long bb = g2 / io.K1;
+          if (bb != ob_b) {
+            if (ob_b >= 0 && io.ob.trace && ob_v != 0.0) atomicAdd(io.ob.trace + ob_b * io.ob.stride + io.ob.col, ob_v);
+            ob_b = bb;
+            ob_v = 0.0;
+          }
+          ob_v += obj_term(io.ob, g2, o, io.K1, y);
         }
+      }
+      if (pre.ok && idx == tid) {
+        if (G.do_fwd && io.D) y = cmul(y, pre.d);
         Xs[i2 * XP + o] = io.Bh ? cadd(y, pre.pb) : y;
         continue;
       }
       const long long k1 = g2 % io.K1;
-      if (G.do_fwd) {
-        y = band_fwd_output(S + i2 * SP, o, KP, ax);
-        if (io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
-      }
+      if (G.do_fwd && io.D) y = cmul(y, __ldg(io.D + k1 * K + o));
       if (io.Bh) {
         C bh = to_c(io.Bh[g2 * K + o], C{});
         if (io.P) bh = cmul(bh, __ldg(io.P + k1 * K + o));
@@ -335,6 +400,10 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
       y = op(g2, o, G.do_fwd ? band_fwd_output(S + i2 * SP, o, KP, ax) : y);
     }
     Xs[i2 * XP + o] = y;
+  }
+  if constexpr (OBJ) {
+    if (G.do_fwd && io.ob.chat && io.ob.trace)
+      warp_group_add(io.ob.trace + io.ob.col, io.ob.stride, ob_b, ob_v);
   }
   __syncthreads();
   if (G.do_inv) {
@@ -348,7 +417,7 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     for (int idx = tid; idx < TR * K; idx += blockDim.x) {
       const int i2 = idx / K, o = idx - i2 * K;
       const long long g2 = row0 + i2;
-      if (g2 < G.rows) io.box_out[g2 * K + o] = Xs[i2 * XP + o];
+      if (g2 < G.rows && io.box_out) io.box_out[g2 * K + o] = Xs[i2 * XP + o];
     }
   }
 }
@@ -439,13 +508,21 @@ __global__ void __launch_bounds__(256) cols_warp_kernel(Geo G, AxisT<float2> ax,
       x[q] = v[0];
     }
   }
+  if constexpr (MULADD) {
+    if (G.do_fwd && io.ob.chat) {   // fused objective trace: box terms of this line (one snapshot)
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < NSET; ++q) v += obj_term(io.ob, line, 32 * q + lane, io.K1, x[q]);
+      if (io.ob.trace) warp_group_add(io.ob.trace + io.ob.col, io.ob.stride, line / io.K1, v);
+    }
+  }
   float2 y[NSET];
 #pragma unroll
   for (int q = 0; q < NSET; ++q) {
     if constexpr (MULADD) {
       y[q] = (G.do_fwd && io.D) ? cmul(x[q], d[q]) : x[q];
       if (io.Bh) y[q] = cadd(y[q], pb[q]);
-      if (!G.do_inv) io.box_out[line * K + 32 * q + lane] = y[q];
+      if (!G.do_inv && io.box_out) io.box_out[line * K + 32 * q + lane] = y[q];
     } else {
       y[q] = op(line, 32 * q + lane, x[q]);
     }
@@ -698,12 +775,18 @@ struct FistaPolicy {
   float2* dp;
   FistaScalars sc;
   float bn;
+  double* tr;       // fused objective: &trace[b][it] (null: off)
+  double tau_b;
   __device__ __forceinline__ FistaPolicy(const EpiFista& e, long long off, int b) {
     cp = e.c + off;
     dp = MOM ? e.d + off : nullptr;
     sc = FistaScalars{e.kscale * e.tau[b], e.a, e.beta_cur, b, e.it, e.first_bad};
     bn = (float)e.beta_next;
+    tr = e.trace ? e.trace + (long long)b * e.trace_stride + e.it : nullptr;
+    tau_b = e.trace ? e.tau[b] : 0.0;
   }
+  __device__ __forceinline__ double* trace_slot() const { return tr; }
+  __device__ __forceinline__ double l1_term(const S& n) const { return tau_b * hypot(n.c.x, n.c.y); }
   __device__ __forceinline__ double kap() const { return sc.kap; }
   __device__ __forceinline__ S load(int o, bool live) const {
     S s;
@@ -817,17 +900,154 @@ struct AdmmSplitPolicy {
   __device__ __forceinline__ float2 first_x(const S& s) const {
     return make_float2((float)(s.z.x - s.r.x), (float)(s.z.y - s.r.y));
   }
+  __device__ __forceinline__ double* trace_slot() const { return nullptr; }
+  __device__ __forceinline__ double l1_term(const S&) const { return 0.0; }
 };
+
+// Tensor-core level 2 of the band inverse (TCI rows tiles, R = 128 threads per line).
+// For each line and register slot j the level-2 sum is
+//   Z_s[j] = sum_m  A0[s][m] * Y[j + KP m],   A0[s][m] = exp(+2 pi i s m / R),
+// i.e. one [R x MO] x [MO x (TR KP)] complex product per tile, shared by every (line, j).
+// As real tf32 GEMMs (K = 8 per step q: m = 4q..4q+3, re then im):
+//   D_re[s][n] = sum_k [A0re | -A0im][s][k] B[n][k],  D_im[s][n] = sum_k [A0im | A0re][s][k] B[n][k]
+// with B[n = ii KP + j] = [Re Y[j + KP m], Im Y[j + KP m]] (m = 4q..4q+3).  Every operand is
+// split into tf32 hi + lo and the product taken as A_hi B_hi + A_lo B_hi + A_hi B_lo (3 MMAs),
+// fp32-grade (tests/test_gpu_tc.py).  D_re sits in TMEM columns [0, N), D_im in [N, 2N),
+// N = TR KP; TMEM lane s belongs to thread s of each line team (warp w reads lanes 32 (w % 4)..).
+struct TcInv {
+  unsigned char* At;   // [MO/4][re_hi | re_lo | im_hi | im_lo][128 x 8 tf32] (K-major, 4 KB each)
+  unsigned char* Bt;   // [MO/4][hi | lo][N x 8 tf32]
+  uint64_t* mbar;      // MMA completion (tcgen05.commit)
+  uint32_t tmem;       // TMEM base column (lane 0)
+  uint32_t phase;      // mbarrier parity of the next completion
+};
+
+template <int KP, int MO, int TR>
+struct TcShape {
+  static constexpr int N = KP * TR;
+  static constexpr int QS = MO / 4;                 // K steps of 8 tf32
+  static constexpr int A_BYTES = QS * 4 * 128 * 32;
+  static constexpr int B_BYTES = QS * 2 * N * 32;
+  static constexpr int COLS = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : (2 * N <= 256 ? 256 : 512)));
+  static_assert(MO % 4 == 0 && MO <= 16, "tensor-core band: MO must be 4, 8, 12 or 16");
+  static_assert(N % 16 == 0 && N <= 256, "tensor-core band: N = KP * TR must be a multiple of 16, <= 256");
+};
+
+// A tiles of the tensor-core level 2 (constant per line length): exp(+2 pi i s m / 128), split.
+template <int MO>
+__device__ __forceinline__ void tc_stage_a(unsigned char* At, int tid, int nthreads) {
+  for (int idx = tid; idx < 128 * MO; idx += nthreads) {
+    const int s = idx % 128, m = idx / 128;
+    const int q = m >> 2, k = m & 3;
+    double sn, cs;
+    sincospi((double)((s * m) % 128) / 64.0, &sn, &cs);   // angle 2 pi s m / 128
+    const float c = (float)cs, si = (float)sn;
+    unsigned char* base = At + q * 4 * 4096;
+    float hi, lo;
+    // D_re row: [cos | -sin];  D_im row: [sin | cos]
+    tc::split_tf32(c, hi, lo);
+    *reinterpret_cast<float*>(base + 0 * 4096 + tc::km_off(s, k)) = hi;
+    *reinterpret_cast<float*>(base + 1 * 4096 + tc::km_off(s, k)) = lo;
+    *reinterpret_cast<float*>(base + 2 * 4096 + tc::km_off(s, 4 + k)) = hi;
+    *reinterpret_cast<float*>(base + 3 * 4096 + tc::km_off(s, 4 + k)) = lo;
+    tc::split_tf32(-si, hi, lo);
+    *reinterpret_cast<float*>(base + 0 * 4096 + tc::km_off(s, 4 + k)) = hi;
+    *reinterpret_cast<float*>(base + 1 * 4096 + tc::km_off(s, 4 + k)) = lo;
+    tc::split_tf32(si, hi, lo);
+    *reinterpret_cast<float*>(base + 2 * 4096 + tc::km_off(s, k)) = hi;
+    *reinterpret_cast<float*>(base + 3 * 4096 + tc::km_off(s, k)) = lo;
+  }
+}
+
+// band value Y[k] of tile line i2 -> B tiles (hi/lo split), k = j + KP m
+template <int KP, int MO, int TR>
+__device__ __forceinline__ void tc_put_b(unsigned char* Bt, int k, int i2, float2 v) {
+  using TSH = TcShape<KP, MO, TR>;
+  const int j = k % KP, m = k / KP;
+  const int q = m >> 2, mm = m & 3;
+  const int n = i2 * KP + j;
+  unsigned char* hi_t = Bt + q * 2 * TSH::N * 32;
+  unsigned char* lo_t = hi_t + TSH::N * 32;
+  float hi, lo;
+  tc::split_tf32(v.x, hi, lo);
+  *reinterpret_cast<float*>(hi_t + tc::km_off(n, mm)) = hi;
+  *reinterpret_cast<float*>(lo_t + tc::km_off(n, mm)) = lo;
+  tc::split_tf32(v.y, hi, lo);
+  *reinterpret_cast<float*>(hi_t + tc::km_off(n, 4 + mm)) = hi;
+  *reinterpret_cast<float*>(lo_t + tc::km_off(n, 4 + mm)) = lo;
+}
+
+// one elected thread: the tile's 6 * MO/4 MMAs, then commit to the mbarrier
+template <int KP, int MO, int TR>
+__device__ __forceinline__ void tc_issue(const TcInv& t) {
+  using TSH = TcShape<KP, MO, TR>;
+  constexpr uint32_t idesc = tc::idesc_tf32<128, TSH::N>();
+  tc::fence_after_sync();
+#pragma unroll
+  for (int q = 0; q < TSH::QS; ++q) {
+    const unsigned char* a = t.At + q * 4 * 4096;
+    const unsigned char* b = t.Bt + q * 2 * TSH::N * 32;
+    const uint64_t are_hi = tc::desc_kmajor(a, tc::KM_LBO, tc::KM_SBO);
+    const uint64_t are_lo = tc::desc_kmajor(a + 4096, tc::KM_LBO, tc::KM_SBO);
+    const uint64_t aim_hi = tc::desc_kmajor(a + 2 * 4096, tc::KM_LBO, tc::KM_SBO);
+    const uint64_t aim_lo = tc::desc_kmajor(a + 3 * 4096, tc::KM_LBO, tc::KM_SBO);
+    const uint64_t b_hi = tc::desc_kmajor(b, tc::KM_LBO, tc::KM_SBO);
+    const uint64_t b_lo = tc::desc_kmajor(b + TSH::N * 32, tc::KM_LBO, tc::KM_SBO);
+    tc::mma_tf32(t.tmem, are_hi, b_hi, idesc, q > 0);
+    tc::mma_tf32(t.tmem, are_lo, b_hi, idesc, 1);
+    tc::mma_tf32(t.tmem, are_hi, b_lo, idesc, 1);
+    tc::mma_tf32(t.tmem + TSH::N, aim_hi, b_hi, idesc, q > 0);
+    tc::mma_tf32(t.tmem + TSH::N, aim_lo, b_hi, idesc, 1);
+    tc::mma_tf32(t.tmem + TSH::N, aim_hi, b_lo, idesc, 1);
+  }
+  tc::commit(t.mbar);
+}
+
+// thread (ii, s): its KP level-2 values of line ii from TMEM
+template <int KP, int MO, int TR>
+__device__ __forceinline__ void tc_read(TcInv& t, int ii, float2 (&a)[KP]) {
+  using TSH = TcShape<KP, MO, TR>;
+  tc::mbar_wait(t.mbar, t.phase);
+  t.phase ^= 1u;
+  tc::fence_after_sync();
+  const uint32_t lane_base = (uint32_t)((threadIdx.x >> 5) & 3) * 32u;
+  const uint32_t col = t.tmem + (lane_base << 16) + (uint32_t)(ii * KP);
+  if constexpr (KP == 32) {
+    float re[32], im[32];
+    tc::tmem_ld32(col, re);
+    tc::tmem_ld32(col + TSH::N, im);
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < KP; ++j) a[j] = make_float2(re[j], im[j]);
+  } else if constexpr (KP == 16) {
+    float re[16], im[16];
+    tc::tmem_ld16(col, re);
+    tc::tmem_ld16(col + TSH::N, im);
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < KP; ++j) a[j] = make_float2(re[j], im[j]);
+  } else {
+    static_assert(KP == 8, "tensor-core band: KP 8, 16 or 32");
+    float re[8], im[8];
+    tc::tmem_ld8(col, re);
+    tc::tmem_ld8(col + TSH::N, im);
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < KP; ++j) a[j] = make_float2(re[j], im[j]);
+  }
+  tc::fence_before_sync();   // these TMEM reads precede the next tile's MMAs (barrier between)
+}
 
 // One tile (TR lines of one snapshot) of the specialised rows pass, complex64 band engine,
 // state policy Pol.  `tile` indexes the tile (and its flag words); with KP2 > 0 and do_fwd,
 // the last tile of a snapshot to arrive runs that snapshot's column pass.  Streaming state /
 // band loads bypass L1 (ld.global.cg): they are read once.
-template <int KP, int R, int MO, typename Pol, bool ZS, int KP2>
+template <int KP, int R, int MO, typename Pol, bool ZS, int KP2, bool TCI = false>
 __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
                                           const typename Pol::Args& epi, unsigned* __restrict__ flags,
                                           const FusedCols& fc, int tile, const float2* tw1s, const float2* tw2s,
-                                          float2* Xs) {
+                                          float2* Xs, TcInv* tci = nullptr) {
+  static_assert(!TCI || (R == 128 && KP2 == 0), "tensor-core tiles: R = 128, no fused column pass");
   using TS = TileShape<KP, R, MO>;
   using St = typename Pol::S;
   constexpr int NT = TS::NT, TR = TS::TR, K = TS::K, XP = TS::XP, PITCH = TS::PITCH, SP = TS::SP;
@@ -878,21 +1098,36 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   }
   if constexpr (PRE_WAIT_READS) pdl_wait();
   if (G.do_inv) {
-    // band tile V[b][k][l20 + ii] -> Xs[ii][k]
+    // band tile V[b][k][l20 + ii] -> Xs[ii][k]   (TCI: -> the MMA's B tiles, tf32 hi/lo)
     for (int idx = tid; idx < TR * K; idx += NT) {
       const int k = idx / TR, i2 = idx % TR;
-      Xs[i2 * XP + k] = __ldcg(io.V + vbase + (long long)k * L2 + i2);
+      const float2 v = __ldcg(io.V + vbase + (long long)k * L2 + i2);
+      if constexpr (TCI) tc_put_b<KP, MO, TR>(tci->Bt, k, i2, v);
+      else Xs[i2 * XP + k] = v;
     }
     if (!EARLY) {
 #pragma unroll
       for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
     }
     if (G.do_fwd && tid < (TR + 31) / 32) live_rows_zero(tid);
+    if constexpr (TCI) tc::fence_async_smem();   // B tiles -> visible to the tensor core
     __syncthreads();
+    if constexpr (TCI) {
+      if (tid == 0) tc_issue<KP, MO, TR>(*tci);
+    }
     unsigned nfl = 0;
+    double l1 = 0.0;          // fused objective: tau_b |c_{t+1}| over this thread's updated points
+    if constexpr (TCI) {
+      // ---- band inverse: level 2 on the tensor core (TcInv), twiddle, level-1 register IDFT
+      tc_read<KP, MO, TR>(*tci, ii, a);
+#pragma unroll
+      for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
+      reg_dft<KP, true>(a);
+    }
     {
       // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT); the band row
       // is read as 16-byte pairs
+      if constexpr (!TCI) {
       const float4* Y4 = reinterpret_cast<const float4*>(Xs + ii * XP);
 #pragma unroll
       for (int j = 0; j < KP; j += 2) {
@@ -913,6 +1148,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
 #pragma unroll
       for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
       reg_dft<KP, true>(a);
+      }
       // ---- fused epilogue, register-pipelined state stream.
       // Warp-level fast path: a clear segment whose 32 points all stay below the threshold
       // stays exactly zero (same test as the per-point fast path below).  One warp AND-reduce
@@ -950,6 +1186,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
           if (active && !(Pol::zero(sb[q]) && fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
             n = pol.update(sb[q], g);
             if (!ZS) pol.store(r * R, n);
+            if (pol.trace_slot()) l1 += pol.l1_term(n);
           }
           if (ZS) {
             if (__any_sync(0xffffffffu, !Pol::zero(n))) {  // segment (still / newly) nonzero: write it whole
@@ -966,6 +1203,11 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       }
     }
     if (ZS && lane == 0) *fw = nfl;
+    if (pol.trace_slot()) {   // whole CTA in one snapshot: one atomic per warp
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      if (lane == 0 && l1 != 0.0) atomicAdd(pol.trace_slot(), l1);
+    }
   } else if (active) {
 #pragma unroll
     for (int r = 0; r < KP; ++r) {
@@ -1061,6 +1303,54 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
   rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs);
+}
+
+// Tensor-core variant of the specialised FISTA/ISTA rows pass (lines of L1 = 128 KP points, band
+// K = KP MO): the level-2 stage of the band inverse runs as kind::tf32 MMAs (TcInv), the rest
+// of rows_tile is unchanged.  Persistent: each CTA stages the constant A tiles, allocates its
+// TMEM columns and initialises its mbarrier once, then walks tiles blockIdx.x, +gridDim.x, ...
+template <int KP, int MO, bool MOM, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    rows_fista_tc_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
+                         int ntiles) {
+  constexpr int R = 128;
+  using TS = TileShape<KP, R, MO>;
+  using TSH = TcShape<KP, MO, TS::TR>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* Xs = reinterpret_cast<float2*>(smem_raw);
+  const float2* tw1s;
+  const float2* tw2s;
+  size_t off = (size_t)(TS::TR * TS::XP + TS::TR * TS::SP) * sizeof(float2);
+  stage_twiddles<KP, R, MO>(ax, reinterpret_cast<float2*>(smem_raw + off), tw1s, tw2s);
+  if constexpr (TS::STAGE_TW) off += (size_t)(KP + MO) * R * sizeof(float2);
+  off = (off + 127) & ~(size_t)127;
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  TcInv t;
+  t.At = smem_raw + off;
+  t.Bt = t.At + TSH::A_BYTES;
+  t.mbar = &mbar;
+  t.phase = 0;
+  tc_stage_a<MO>(t.At, threadIdx.x, TS::NT);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc(&tmem_base, TSH::COLS);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  t.tmem = tmem_base;
+  const FusedCols nofc{};
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs, &t);
+    __syncthreads();   // Xs / S / B tiles and TMEM are reused by the next tile
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (threadIdx.x < 32) tc::tmem_dealloc(t.tmem, TSH::COLS);
 }
 
 // ---------------------------------------------------------------- ADMM, spectral dual split

@@ -354,8 +354,6 @@ def _fista_like(problem: LassoProblem, config: SolverConfig, momentum: bool) -> 
     stream = _stream_ptr(op.device)
     record = config.record_objective
     y_norm = _require_y_norm(problem) if record else None
-    if record and problem._b_dense is None:
-        raise InvalidArgumentError("recording the objective trace needs the dense b (keep_b=True)")
     precompute = time.perf_counter() - t0
     T = config.iterations
     trace = np.zeros((problem.batch, T if record else 0))
@@ -365,9 +363,22 @@ def _fista_like(problem: LassoProblem, config: SolverConfig, momentum: bool) -> 
                              c.data_ptr(), d.data_ptr() if d is not None else None,
                              first_bad.data_ptr(), ws.data_ptr(), stream)
     ev0.record()
+    fused = False
+    if record and extra is None and config.initial_c is None:
+        # objective trace fused into the pass kernels (device reductions, one call)
+        tr = torch.empty((problem.batch, T), dtype=torch.float64, device=c.device)
+        rc = _lib.lib.bccb_fista_run_traced(op._plan, problem.batch, T, float(mu), tau_dev.data_ptr(),
+                                            bhat.data_ptr(), c.data_ptr(), d.data_ptr() if d is not None else None,
+                                            first_bad.data_ptr(), tr.data_ptr(), ws.data_ptr(), stream)
+        if rc != _lib.ERR_UNSUPPORTED:
+            _lib.check(rc)
+            fused = True
     if not record:
         _lib.check(_lib.lib.bccb_fista_run(*args(0, T)))
-    else:
+    elif not fused:
+        # per-iteration slow path (generic operators, b off the box, small grids)
+        if problem._b_dense is None:
+            raise InvalidArgumentError("recording the objective trace needs the dense b (keep_b=True)")
         for t in range(T):
             _lib.check(_lib.lib.bccb_fista_run(*args(t, 1)))
             trace[:, t] = _objective(problem, c, tau_dev, y_norm)
@@ -375,6 +386,9 @@ def _fista_like(problem: LassoProblem, config: SolverConfig, momentum: bool) -> 
     ev1.synchronize()
     elapsed = ev0.elapsed_time(ev1) / 1e3
     _check_divergence(first_bad)
+    if fused:
+        yn = torch.as_tensor(y_norm, dtype=torch.float64, device=c.device).reshape(-1, 1)
+        trace = (tr + yn).cpu().numpy()
     return SolverResult(
         estimate=_finish(problem, c),
         objective_trace=trace[0] if problem._squeeze else trace,

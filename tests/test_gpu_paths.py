@@ -313,3 +313,33 @@ def test_pdl_bitwise_across_solvers(tmp_path, cfg, solver, iters):
     assert np.isfinite(outs[0]).all() and np.count_nonzero(outs[0]) > 0
     np.testing.assert_array_equal(outs[0], outs[2])
     np.testing.assert_array_equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("cfg,nsnap,iters", [(4, 3, 120), (5, 1, 40)])
+def test_tensor_core_rows_engine_matches_cuda_core_engine(tmp_path, cfg, nsnap, iters):
+    """The tensor-core rows engine (tcgen05 kind::tf32 level-2 stage of the band inverse,
+    3-pass hi/lo split) against the CUDA-core engine (BCCB_ROWS_TC=0) and the float64 oracle:
+    equal to fp32 rounding, identical top-K (fresh processes: the engine is chosen once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(_PDL_SCRIPT.replace("range(9)", f"range({nsnap})"))
+    outs = []
+    for env in ({"BCCB_ROWS_TC": "1"}, {"BCCB_ROWS_TC": "0"}):
+        out = tmp_path / f"est{len(outs)}.npy"
+        subprocess.run([sys.executable, str(script), root, str(out), str(cfg), "fista", str(iters)], check=True,
+                       env=dict(os.environ, **env), timeout=900)
+        outs.append(np.load(out))
+    w = scenes.workload(cfg)
+    geom, ys, _ = scenes.make_scene(w, range(nsnap))
+    m1, m2 = geom.occupied_coordinates()
+    eig_t = np.ascontiguousarray(orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2).T)
+    for s_, y in enumerate(ys):
+        b = orc.adjoint_fft(m1, m2, w.l1, w.l2, y)
+        ref = orc.fista(eig_t, b, w.tau_fraction * np.abs(b).max(), 1.0 / (w.l1 * w.l2), iters)
+        e_tc, e_cc = orc.rel_l2(outs[0][s_], ref), orc.rel_l2(outs[1][s_], ref)
+        assert e_tc < 1e-5 and e_cc < 1e-5, (e_tc, e_cc)
+        assert orc.rel_l2(outs[0][s_], outs[1][s_]) < 1e-5
+        np.testing.assert_array_equal(orc.topk(outs[0][s_], w.targets), orc.topk(ref, w.targets))

@@ -14,7 +14,7 @@ import torch
 import paper_2509_13592_b200 as bb
 from conftest import dense_estimates, load_golden
 from oracle import bccb_oracle as orc
-from paper_2509_13592_b200 import scenes
+from paper_2509_13592_b200 import _lib, scenes
 
 pytestmark = pytest.mark.gpu
 PARITY = 1e-4
@@ -254,3 +254,37 @@ def test_config4_full_batch_snapshot0():
     idx, _ = bb.topk_peaks(est, w.targets)
     np.testing.assert_array_equal(np.sort(idx.cpu().numpy()[0]), np.sort(g["topk"][0]))
     assert np.isfinite(est).all()
+
+
+@pytest.mark.parametrize("cfg,nsnap,iters,solver", [(2, 3, 60, "fista"), (2, 2, 40, "ista"), (4, 2, 30, "fista")])
+def test_fused_objective_trace(cfg, nsnap, iters, solver):
+    """record_objective=True on a specialised grid runs ONE fused call: tau ||c||_1 summed by the
+    rows pass, -2 Re<b,c> + <c,Gc> on the spectral box by the column pass (Parseval, C_t from the
+    FISTA point's FFT2 by linearity), no per-iteration host loop.  Checked against the
+    reference identity (solvers.py:233-242) on float64 oracle iterates."""
+    w = scenes.workload(cfg)
+    geom, ys, _ = scenes.make_scene(w, range(nsnap))
+    op = bb.gram_operator(geom, w.l1, w.l2)
+    m1, m2 = geom.occupied_coordinates()
+    bs = np.stack([orc.adjoint_fft(m1, m2, w.l1, w.l2, y) for y in ys])
+    taus = np.array([w.tau_fraction * np.abs(b).max() for b in bs])
+    ynorms = np.real(np.einsum("ij,ij->i", ys.conj(), ys))
+    mu = 1.0 / (w.l1 * w.l2)
+    prob = bb.LassoProblem(op, bs, taus, y_norm_sq=ynorms)
+    solve = bb.fista_solve if solver == "fista" else bb.ista_solve
+    conf = bb.SolverConfig(iterations=iters, step_size_mu=mu, record_objective=True)
+    calls0 = _lib.lib.bccb_launch_count()
+    res = solve(prob, conf)
+    launches = _lib.lib.bccb_launch_count() - calls0
+    assert res.objective_trace.shape == (nsnap, iters)
+    assert launches < 6 * iters + 40          # one fused call, not a per-iteration loop
+    plain = solve(bb.LassoProblem(op, bs, taus), bb.SolverConfig(iterations=iters, step_size_mu=mu))
+    np.testing.assert_array_equal(res.estimate, plain.estimate)   # recording does not perturb the iterate
+    eig_t = np.ascontiguousarray(orc.gram_eigenvalues_exact(geom.occupancy, w.l1, w.l2).T)
+    run = orc.fista if solver == "fista" else orc.ista
+    for s_ in range(nsnap):
+        for t in (1, iters // 3, iters):
+            c = run(eig_t, bs[s_], taus[s_], mu, t)
+            expect = (ynorms[s_] - 2 * np.real(np.vdot(bs[s_], c)) + np.real(np.vdot(c, orc.matvec(eig_t, c)))
+                      + taus[s_] * np.abs(c).sum())
+            np.testing.assert_allclose(res.objective_trace[s_, t - 1], expect, rtol=2e-6)
