@@ -99,6 +99,15 @@ int bccb_spectrum_box(bccb_plan_t plan, int batch, const void* x, void* out_box,
 int bccb_synthesize(bccb_plan_t plan, int batch, const void* box, float scale, const void* x,
                     float alpha, void* out, float* maxabs, void* workspace, void* stream);
 
+/* complex128 counterparts of bccb_spectrum_box / bccb_synthesize (x, out_box, box, out:
+ * device complex128), on the float64 band engine: the eigenvalue transform of
+ * bccb_from_first_column (bccb.py:93-105: fft2 of the first column) and its inverse
+ * bccb_first_column (bccb.py:151-153) at float64 accuracy. */
+int bccb_spectrum_box_z(bccb_plan_t plan, int batch, const void* x, void* out_box, void* workspace,
+                        void* stream);
+int bccb_synthesize_z(bccb_plan_t plan, int batch, const void* box, double scale, void* out,
+                      void* workspace, void* stream);
+
 /* A^H y for a batch of snapshots (Gram plans only).
  * Replaces apply_adjoint (dictionary.py:129-136) on the grid f = -1/2 + l/L
  * (dictionary.py:41-45) plus the per-snapshot max|b| of the tau rule

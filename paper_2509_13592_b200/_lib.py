@@ -45,6 +45,8 @@ SIGNATURES = {
     "bccb_matvec_z": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "bccb_spectrum_box": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "bccb_synthesize": (_i, [_vp, _i, _vp, _f, _vp, _f, _vp, _vp, _vp, _vp]),
+    "bccb_spectrum_box_z": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "bccb_synthesize_z": (_i, [_vp, _i, _vp, _d, _vp, _vp, _vp]),
     "bccb_adjoint": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bccb_fista_run": (_i, [_vp, _i, _i, _i, _d] + [_vp] * 8),
     "bccb_fista_run_traced": (_i, [_vp, _i, _i, _d] + [_vp] * 8),

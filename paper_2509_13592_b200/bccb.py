@@ -13,6 +13,7 @@ dimension.  Arithmetic is complex64 on the GPU (BASELINE.json north_star).
 """
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -68,7 +69,7 @@ class BccbOperator:
         self.l1, self.l2 = int(l1), int(l2)
         self.device = _device_index(device)
         self._eig_host = None
-        self._ws = {}
+        self._ws = threading.local()    # scratch per calling thread
         handle = ctypes.c_void_p()
         if _gram is not None:
             m1c, m2c, occ = _gram
@@ -155,11 +156,19 @@ class BccbOperator:
         return m
 
     def workspace(self, batch: int) -> torch.Tensor:
-        ws = self._ws.get(batch)
+        """Scratch for one call of `batch` snapshots.  Cached per calling thread and CUDA
+        stream, so concurrent matvecs / solves on one operator never share intermediates
+        (reference contract SPEC.md:325: scratch per call or per thread)."""
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        cache = getattr(self._ws, "cache", None)
+        if cache is None:
+            cache = self._ws.cache = {}
+        ws = cache.get((batch, stream))
         if ws is None:
             nbytes = int(_lib.lib.bccb_workspace_bytes(self._plan, batch))
             ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
-            self._ws = {batch: ws}  # keep one cached size
+            cache.clear()                  # keep one size per thread
+            cache[(batch, stream)] = ws
         return ws
 
     def __repr__(self) -> str:
@@ -218,11 +227,12 @@ def bccb_from_first_column(col, l1: int, l2: int, device=None) -> BccbOperator:
         raise InvalidArgumentError(f"first column length {values.size} does not match L1*L2 = {l1 * l2}")
     dev = _device_index(device)
     probe = BccbOperator(l1, l2, device=dev, _box=np.ones((l1, l2)), _lam_out=0.0)
-    x = _as_device_c64(values, dev)
-    box = torch.empty((1, probe.k1, probe.k2), dtype=torch.complex64, device=x.device)
-    _lib.check(_lib.lib.bccb_spectrum_box(probe._plan, 1, x.data_ptr(), box.data_ptr(),
-                                          probe.workspace(1).data_ptr(), _stream_ptr(dev)))
-    eig = box[0].to(torch.complex128).cpu().numpy()  # [k1][k2] = eigenvalues[k1, k2]
+    x = torch.from_numpy(np.ascontiguousarray(values, dtype=np.complex128)).to(f"cuda:{dev}")
+    box = torch.empty((1, probe.k1, probe.k2), dtype=torch.complex128, device=x.device)
+    # float64 band engine: the reference computes fft2 in float64 (bccb.py:104)
+    _lib.check(_lib.lib.bccb_spectrum_box_z(probe._plan, 1, x.data_ptr(), box.data_ptr(),
+                                            probe.workspace(1).data_ptr(), _stream_ptr(dev)))
+    eig = box[0].cpu().numpy()  # [k1][k2] = eigenvalues[k1, k2]
     return BccbOperator(l1, l2, eig, device=dev)
 
 
@@ -298,11 +308,12 @@ def bccb_first_column(op: BccbOperator) -> FirstColumn:
     """Recover the first column by inverse 2D DFT on the GPU (bccb.py:151-153)."""
     dev = op.device
     lo = op.lam_out if not op.is_full_box else 0.0
-    box = torch.from_numpy(np.ascontiguousarray((op.box - lo)[None], dtype=np.complex64)).to(f"cuda:{dev}")
-    out = torch.empty((1, op.dimension), dtype=torch.complex64, device=box.device)
+    box = torch.from_numpy(np.ascontiguousarray((op.box - lo)[None], dtype=np.complex128)).to(f"cuda:{dev}")
+    out = torch.empty((1, op.dimension), dtype=torch.complex128, device=box.device)
     scale = 1.0 / op.dimension
-    _lib.check(_lib.lib.bccb_synthesize(op._plan, 1, box.data_ptr(), scale, None, 0.0, out.data_ptr(),
-                                        None, op.workspace(1).data_ptr(), _stream_ptr(dev)))
-    values = out[0].cpu().numpy().astype(np.complex128)
+    # float64 band engine (the reference's ifft2, bccb.py:153)
+    _lib.check(_lib.lib.bccb_synthesize_z(op._plan, 1, box.data_ptr(), scale, out.data_ptr(),
+                                          op.workspace(1).data_ptr(), _stream_ptr(dev)))
+    values = out[0].cpu().numpy()
     values[0] += lo
     return FirstColumn(values)

@@ -230,11 +230,9 @@ struct bccb_plan_s {
   int* occ_dev = nullptr;          // [3][M]: m1, m2 (reduced mod L1 / L2), (m1 + m2) & 1
   int occ_alias = 0;               // some occupied cells alias (M1 > L1 or M2 > L2)
   static constexpr int MAX_SUB = 8;
-  cudaStream_t aux[MAX_SUB - 1] = {};   // extra streams of the sub-batch split (created lazily)
-  double* beta_dev = nullptr;      // momentum table of the small-grid persistent solver
-  size_t beta_cap = 0;
-  std::vector<double> beta_host;
-  cudaEvent_t ev_fork = nullptr, ev_join[MAX_SUB - 1] = {};
+  // Threading: after creation a plan is read-only.  Everything a call
+  // mutates lives in the caller's workspace, in per-thread state (the sub-batch streams and
+  // events, SubStreams) or in the process-wide, grow-only momentum table (beta_table).
   bool full() const { return ax1.K == L1 && ax2.K == L2; }
 };
 
@@ -334,12 +332,6 @@ static void free_plan(bccb_plan_s* p) {
   free_axis(p->ax2);
   cudaFree(p->lam_box_dev);
   cudaFree(p->occ_dev);
-  for (int i = 0; i < bccb_plan_s::MAX_SUB - 1; ++i) {
-    if (p->aux[i]) cudaStreamDestroy(p->aux[i]);
-    if (p->ev_join[i]) cudaEventDestroy(p->ev_join[i]);
-  }
-  cudaFree(p->beta_dev);
-  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   cudaSetDevice(cur);
   delete p;
 }
@@ -1418,13 +1410,23 @@ extern "C" int bccb_substreams_for(bccb_plan_t p, int batch) {
   return sub_batches(p, batch);
 }
 
-static int ensure_aux_streams(bccb_plan_s* p, int n) {
-  if (!p->ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+// Sub-batch streams and fork/join events: per calling thread and device, so concurrent solves
+// on one plan from different threads never share an event (created lazily, reused).
+struct SubStreams {
+  cudaStream_t aux[bccb_plan_s::MAX_SUB - 1] = {};
+  cudaEvent_t fork = nullptr, join[bccb_plan_s::MAX_SUB - 1] = {};
+};
+static thread_local SubStreams t_sub[64];
+
+static int ensure_aux_streams(const bccb_plan_s* p, int n, SubStreams** out) {
+  SubStreams& ss = t_sub[p->device & 63];
+  if (!ss.fork) CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
   for (int i = 0; i < n - 1; ++i) {
-    if (p->aux[i]) continue;
-    CUDA_TRY(cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming));
+    if (ss.aux[i]) continue;
+    CUDA_TRY(cudaStreamCreateWithFlags(&ss.aux[i], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming));
   }
+  *out = &ss;
   return BCCB_OK;
 }
 
@@ -1460,22 +1462,39 @@ static bool small_supported(const bccb_plan_s* p, const void* extra, bool mom) {
 }
 
 // momentum coefficients beta_t, t <= t_end, in a plan-owned device table (persistent solvers)
-static int upload_beta(bccb_plan_s* p, int t_end, cudaStream_t st) {
-  if (p->beta_cap < (size_t)t_end + 1) {
-    cudaFree(p->beta_dev);
-    p->beta_dev = nullptr;
-    p->beta_cap = std::max<size_t>((size_t)t_end + 1, 1024);
-    CUDA_TRY(cudaMalloc(&p->beta_dev, p->beta_cap * sizeof(double)));
+// FISTA momentum table beta[0..t_end] of the persistent small-grid / cluster solvers
+// (beta_t = (alpha_{t-1} - 1) / alpha_t, solvers.py:294-337).  The sequence does not depend on
+// the call, so one process-wide table per device serves every plan and thread; it only grows
+// (filled synchronously before its pointer is published) and retired tables are kept, so a
+// kernel still reading an older one stays valid.
+static std::mutex g_beta_mu;
+struct BetaTable {
+  double* dev = nullptr;
+  size_t cap = 0;
+  std::vector<double*> retired;
+};
+static BetaTable g_beta[64];
+
+static int beta_table(const bccb_plan_s* p, int t_end, const double** out) {
+  std::lock_guard<std::mutex> lk(g_beta_mu);
+  BetaTable& bt = g_beta[p->device & 63];
+  if (bt.cap < (size_t)t_end + 1) {
+    const size_t cap = std::max<size_t>({(size_t)t_end + 1, 2 * bt.cap, 1024});
+    std::vector<double> host(cap, 0.0);
+    double alpha = 1.0;
+    for (size_t t = 1; t < cap; ++t) {
+      const double an = 0.5 * (std::sqrt(1.0 + 4.0 * alpha * alpha) + 1.0);
+      host[t] = (alpha - 1.0) / an;
+      alpha = an;
+    }
+    double* dev = nullptr;
+    CUDA_TRY(cudaMalloc(&dev, cap * sizeof(double)));
+    CUDA_TRY(cudaMemcpy(dev, host.data(), cap * sizeof(double), cudaMemcpyHostToDevice));
+    if (bt.dev) bt.retired.push_back(bt.dev);
+    bt.dev = dev;
+    bt.cap = cap;
   }
-  p->beta_host.assign((size_t)t_end + 1, 0.0);
-  double alpha = 1.0;
-  for (int t = 1; t <= t_end; ++t) {
-    const double an = 0.5 * (std::sqrt(1.0 + 4.0 * alpha * alpha) + 1.0);
-    p->beta_host[t] = (alpha - 1.0) / an;
-    alpha = an;
-  }
-  CUDA_TRY(cudaMemcpyAsync(p->beta_dev, p->beta_host.data(), p->beta_host.size() * sizeof(double),
-                           cudaMemcpyHostToDevice, st));
+  *out = bt.dev;
   return BCCB_OK;
 }
 
@@ -1492,14 +1511,15 @@ static bool cluster_supported(const bccb_plan_s* p, const void* extra) {
 
 static int launch_cluster64(bccb_plan_s* p, int batch, int first, int iters, const EpiFista& e, const float2* D,
                             const float2* P, const float2* Bh, cudaStream_t st) {
-  int rc = upload_beta(p, first + iters, st);
+  const double* beta_dev = nullptr;
+  int rc = beta_table(p, first + iters, &beta_dev);
   if (rc) return rc;
   ClusterArgs A;
   A.D = D;
   A.P = P;
   A.Bh = Bh;
   A.epi = e;
-  A.beta = p->beta_dev;
+  A.beta = beta_dev;
   A.K1 = p->ax1.K;
   A.K2 = p->ax2.K;
   A.iterations = iters;
@@ -1516,7 +1536,8 @@ static int launch_cluster64(bccb_plan_s* p, int batch, int first, int iters, con
 static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const EpiFista& e, const float2* D,
                         const float2* P, const float2* Bh, cudaStream_t st) {
   const bool mom = e.momentum != 0;
-  int rc0 = upload_beta(p, first + iters, st);
+  const double* beta_dev = nullptr;
+  int rc0 = beta_table(p, first + iters, &beta_dev);
   if (rc0) return rc0;
   SmallArgs A;
   A.ax1 = p->ax1.dev<float2>();
@@ -1527,7 +1548,7 @@ static int launch_small(bccb_plan_s* p, int batch, int first, int iters, const E
   A.cio.Bh = Bh;
   A.cio.K1 = p->ax1.K;
   A.epi = e;
-  A.beta = p->beta_dev;
+  A.beta = beta_dev;
   A.L1 = p->L1;
   A.L2 = p->L2;
   A.K1 = p->ax1.K;
@@ -1634,7 +1655,8 @@ static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int ite
   // column pass and kernel tails overlap the other half's rows pass.  Snapshots are
   // independent, so the arithmetic is identical to one stream (bitwise).
   const int nsub = sub_batches(p, batch);
-  if (nsub > 1 && (rc = ensure_aux_streams(p, nsub))) return rc;
+  SubStreams* ss = nullptr;
+  if (nsub > 1 && (rc = ensure_aux_streams(p, nsub, &ss))) return rc;
   struct Sub {
     int b0, nb;
     cudaStream_t st;
@@ -1645,7 +1667,7 @@ static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int ite
     Sub& u = sub[q];
     u.b0 = (int)((long long)batch * q / nsub);
     u.nb = (int)((long long)batch * (q + 1) / nsub) - u.b0;
-    u.st = q == 0 ? st : p->aux[q - 1];
+    u.st = q == 0 ? st : ss->aux[q - 1];
     u.w = w;
     const long long inter = (long long)u.b0 * p->ax1.K * p->L2;
     u.w.U = (float2*)w.U + inter;
@@ -1700,8 +1722,8 @@ static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int ite
               : launch_rows_fista(p, u.nb, inv, fwd, u.w, u.e, u.st);
   };
   if (nsub > 1) {
-    CUDA_TRY(cudaEventRecord(p->ev_fork, st));
-    for (int q = 1; q < nsub; ++q) CUDA_TRY(cudaStreamWaitEvent(p->aux[q - 1], p->ev_fork, 0));
+    CUDA_TRY(cudaEventRecord(ss->fork, st));
+    for (int q = 1; q < nsub; ++q) CUDA_TRY(cudaStreamWaitEvent(ss->aux[q - 1], ss->fork, 0));
   }
   for (int q = 0; q < nsub; ++q)
     if ((rc = rows(q, false, true))) return rc;
@@ -1731,8 +1753,8 @@ static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int ite
   for (int q = 0; q < nsub; ++q)
     if (zs && (rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].e.c, sub[q].e.d, sub[q].st, tcr))) return rc;
   for (int q = 1; q < nsub; ++q) {
-    CUDA_TRY(cudaEventRecord(p->ev_join[q - 1], p->aux[q - 1]));
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join[q - 1], 0));
+    CUDA_TRY(cudaEventRecord(ss->join[q - 1], ss->aux[q - 1]));
+    CUDA_TRY(cudaStreamWaitEvent(st, ss->join[q - 1], 0));
   }
   return BCCB_OK;
 }
@@ -1860,7 +1882,8 @@ static int admm_run_split(bccb_plan_s* p, int batch, int first_iteration, int it
   // Not with c_last: its complex128 synthesis borrows the whole U region mid-iteration, which a
   // concurrent part's column pass still reads.
   const int nsub = c_last ? 1 : sub_batches(p, batch);
-  if (nsub > 1 && (rc = ensure_aux_streams(p, nsub))) return rc;
+  SubStreams* ss = nullptr;
+  if (nsub > 1 && (rc = ensure_aux_streams(p, nsub, &ss))) return rc;
   struct Sub {
     int b0, nb;
     cudaStream_t st;
@@ -1873,7 +1896,7 @@ static int admm_run_split(bccb_plan_s* p, int batch, int first_iteration, int it
     Sub& u = sub[q];
     u.b0 = (int)((long long)batch * q / nsub);
     u.nb = (int)((long long)batch * (q + 1) / nsub) - u.b0;
-    u.st = q == 0 ? st : p->aux[q - 1];
+    u.st = q == 0 ? st : ss->aux[q - 1];
     const long long inter = (long long)u.b0 * p->ax1.K * p->L2;
     const long long boxo = (long long)u.b0 * p->ax1.K * p->ax2.K;
     const long long off = (long long)u.b0 * p->L1 * p->L2;
@@ -1896,8 +1919,8 @@ static int admm_run_split(bccb_plan_s* p, int batch, int first_iteration, int it
     u.op.vs = (double2*)u.w.vs;
   }
   if (nsub > 1) {
-    CUDA_TRY(cudaEventRecord(p->ev_fork, st));
-    for (int q = 1; q < nsub; ++q) CUDA_TRY(cudaStreamWaitEvent(p->aux[q - 1], p->ev_fork, 0));
+    CUDA_TRY(cudaEventRecord(ss->fork, st));
+    for (int q = 1; q < nsub; ++q) CUDA_TRY(cudaStreamWaitEvent(ss->aux[q - 1], ss->fork, 0));
   }
   const int t_end = first_iteration + iterations;
   for (int q = 0; q < nsub; ++q)
@@ -1925,8 +1948,8 @@ static int admm_run_split(bccb_plan_s* p, int batch, int first_iteration, int it
   for (int q = 0; q < nsub; ++q)
     if ((rc = launch_zero_segments(p, sub[q].nb, sub[q].w, sub[q].z, sub[q].v, sub[q].st))) return rc;
   for (int q = 1; q < nsub; ++q) {
-    CUDA_TRY(cudaEventRecord(p->ev_join[q - 1], p->aux[q - 1]));
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join[q - 1], 0));
+    CUDA_TRY(cudaEventRecord(ss->join[q - 1], ss->aux[q - 1]));
+    CUDA_TRY(cudaStreamWaitEvent(st, ss->join[q - 1], 0));
   }
   // v = r + IFFT2u(vs)
   if ((rc = launch_cols_box_z(p, batch, w, (const double2*)w.vs, st))) return rc;
@@ -1991,7 +2014,7 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
 extern "C" size_t bccb_topk_workspace_bytes(int batch, long long length, int k) {
   if (batch < 1 || length < 1 || k < 1) return 0;
   const int nchunk = topk_chunks(batch, length);
-  return (size_t)batch * nchunk * pow2_ceil(k) * sizeof(unsigned long long) + 256;
+  return (size_t)batch * nchunk * pow2_ceil(k) * sizeof(TKey) + 256;
 }
 
 extern "C" int bccb_topk(int batch, long long length, const void* values, int is_double, int k,
@@ -2004,7 +2027,7 @@ extern "C" int bccb_topk(int batch, long long length, const void* values, int is
   if (!values || !idx || !workspace) return fail(BCCB_ERR_INVALID, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
   const int nchunk = topk_chunks(batch, length);
-  unsigned long long* cand = (unsigned long long*)workspace;
+  TKey* cand = (TKey*)workspace;
   const int kt = std::max(4, pow2_ceil(k));
 #define TOPK_CASE(KT)                                                                            \
   case KT:                                                                                       \
@@ -2025,4 +2048,36 @@ extern "C" int bccb_topk(int batch, long long length, const void* values, int is
 #undef TOPK_CASE
   LAUNCH_CHECK();
   return BCCB_OK;
+}
+
+// ------------------------------------------------------------------ complex128 spectrum / synthesis
+// fft2 restricted to the box and the inverse synthesis on the complex128 band engine: the
+// float64 paths of bccb_from_first_column / bccb_first_column (bccb.py:93-105, 151-153), pinned
+// at rtol 1e-11 by the reference's pkg/tests/test_bccb.py:99-107.
+extern "C" int bccb_spectrum_box_z(bccb_plan_t p, int batch, const void* x, void* out_box, void* workspace,
+                                   void* stream) {
+  EntryScope entry_scope_;
+  int rc = check_common(p, batch, workspace);
+  if (rc) return rc;
+  if (!x || !out_box) return fail(BCCB_ERR_INVALID, "x / out_box is NULL");
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace w = carve(p, batch, workspace);
+  EpiVector<double2> e{(const double2*)x, nullptr, nullptr, 0.0, 1.0};
+  if ((rc = launch_rows_vector<double2>(p, batch, false, true, w, e, st))) return rc;
+  return launch_cols<double2>(p, batch, true, false, w, nullptr, nullptr, nullptr, (double2*)out_box, st);
+}
+
+extern "C" int bccb_synthesize_z(bccb_plan_t p, int batch, const void* box, double scale, void* out,
+                                 void* workspace, void* stream) {
+  EntryScope entry_scope_;
+  int rc = check_common(p, batch, workspace);
+  if (rc) return rc;
+  if (!box || !out) return fail(BCCB_ERR_INVALID, "box / out is NULL");
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace w = carve(p, batch, workspace);
+  if ((rc = launch_cols_box_z(p, batch, w, (const double2*)box, st))) return rc;
+  EpiVector<double2> e{nullptr, (double2*)out, nullptr, 0.0, scale};
+  return launch_rows_vector<double2>(p, batch, true, false, w, e, st);
 }

@@ -512,8 +512,9 @@ def topk_peaks(values, k: int):
 def extract_support(c_hat, grid1, grid2, threshold_fraction: float):
     """Entries with |c| >= frac * max|c|, by descending magnitude (solvers.py:476-507).
 
-    Selection runs on the GPU through the top-k kernel; when more than 64 entries
-    clear the threshold the ordering falls back to a device-side stable sort.
+    Selection runs on the GPU through the top-k kernel (float64 magnitudes, ties to the lower
+    index); the threshold is applied to float64 magnitudes exactly as the reference does.  When
+    more than 64 entries clear the threshold the ordering falls back to a device-side stable sort.
     """
     if not 0.0 < threshold_fraction < 1.0:
         raise InvalidArgumentError("threshold fraction must lie strictly between 0 and 1")
@@ -522,16 +523,17 @@ def extract_support(c_hat, grid1, grid2, threshold_fraction: float):
     if shape != (n,):
         raise InvalidArgumentError("coefficient length does not match the grids")
     host = c_hat.detach().cpu().numpy() if isinstance(c_hat, torch.Tensor) else np.asarray(c_hat)
+    host = host.astype(np.complex128, copy=False)
     k = min(64, n)
-    idx, mag = topk_peaks(c_hat if isinstance(c_hat, torch.Tensor) else host.astype(np.complex128), k)
-    idx = idx[0].cpu().numpy()
-    mag = mag[0].cpu().numpy().astype(np.float64)
+    idx, _ = topk_peaks(c_hat if isinstance(c_hat, torch.Tensor) else host, k)
+    idx = idx[0].cpu().numpy().astype(np.int64)
+    mag = np.abs(host[idx])                       # float64, as np.abs in the reference
     peak = float(mag[0])
     if peak == 0.0:
         return []
     thr = threshold_fraction * peak
     if k < n and mag[-1] >= thr:
-        dev = torch.as_tensor(np.abs(host.astype(np.complex128))).cuda()
+        dev = torch.as_tensor(np.abs(host)).cuda()
         order = torch.sort(-dev, stable=True).indices
         keep = (dev[order] >= thr).cpu().numpy()
         kept = order.cpu().numpy()[keep]

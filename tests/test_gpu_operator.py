@@ -167,3 +167,71 @@ def test_extract_support_matches_reference(small):
     c[10] = 2.0
     sup = bb.extract_support(c, bb.make_uniform_grid(16), bb.make_uniform_grid(16), 0.1)
     assert len(sup) == 256 and sup[0][2] == 2.0
+
+
+def _dense_from_first_column(col, l1, l2):
+    """Dense BCCB expansion by modular index arithmetic: entry (i, j) = col[(i1 - j1) mod L1 +
+    ((i2 - j2) mod L2) L1] (the reference test's independent oracle, test_bccb.py:45-54)."""
+    i = np.arange(l1 * l2)
+    i1, i2 = i % l1, i // l1
+    return col[((i1[:, None] - i1[None, :]) % l1) + ((i2[:, None] - i2[None, :]) % l2) * l1]
+
+
+def test_first_column_operators_match_dense_at_reference_tolerance():
+    """pkg/tests/test_bccb.py:99-107 through the drop-in: 20 random first columns (L1, L2 in
+    1..8), bccb_from_first_column on the float64 band engine, numpy matvec vs the dense
+    expansion at rtol 1e-11; bccb_first_column recovers the column at the same precision."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        l1, l2 = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        col = rng.standard_normal(l1 * l2) + 1j * rng.standard_normal(l1 * l2)
+        op = bb.bccb_from_first_column(col, l1, l2)
+        c = rng.standard_normal(l1 * l2) + 1j * rng.standard_normal(l1 * l2)
+        np.testing.assert_allclose(bb.bccb_matvec(op, c), _dense_from_first_column(col, l1, l2) @ c,
+                                   rtol=1e-11, atol=1e-12)
+        np.testing.assert_allclose(bb.bccb_first_column(op).values, col, rtol=1e-11, atol=1e-12)
+    # larger generic shapes of the golden fixture: eigenvalues at float64 accuracy
+    small = load_golden("small")
+    for l1, l2 in small["generic_shapes"]:
+        l1, l2 = int(l1), int(l2)
+        op = bb.bccb_from_first_column(small[f"g{l1}x{l2}_col"], l1, l2)
+        assert orc.rel_l2(op.eigenvalues, small[f"g{l1}x{l2}_eig"]) < 1e-13
+
+
+def test_concurrent_matvec_and_solves_on_one_operator():
+    """an operator is shareable and matvec may run concurrently.  Two threads,
+    each on its own CUDA stream, apply one config-2 operator and run FISTA solves on it at the
+    same time; every result equals the single-threaded one bitwise (per-thread workspace and
+    per-thread sub-batch streams)."""
+    import threading
+    w = scenes.workload(2)
+    geom, ys, _ = scenes.make_scene(w, range(8))
+    op = bb.gram_operator(geom, w.l1, w.l2)
+    rng = np.random.default_rng(5)
+    xs = [torch.as_tensor(rng.standard_normal((4, w.grid_points)) + 1j * rng.standard_normal((4, w.grid_points)),
+                          dtype=torch.complex64).cuda() for _ in range(2)]
+    conf = bb.SolverConfig(iterations=80, step_size_mu=1.0 / w.grid_points)
+    probs = [bb.LassoProblem.from_measurements(op, ys[4 * i:4 * i + 4], tau_fraction=w.tau_fraction) for i in range(2)]
+
+    def work(i):
+        return bb.bccb_matvec(op, xs[i]).cpu().numpy(), bb.fista_solve(probs[i], conf).estimate
+
+    ref = [work(i) for i in range(2)]
+    out = [None, None]
+
+    def run(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                mv, est = work(i)
+                out[i] = (mv, est)
+            s.synchronize()
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for i in range(2):
+        np.testing.assert_array_equal(out[i][0], ref[i][0])
+        np.testing.assert_array_equal(out[i][1], ref[i][1])
