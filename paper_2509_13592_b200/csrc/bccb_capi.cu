@@ -1,6 +1,7 @@
 // C ABI + launch sequencing for the B200-native BCCB Gram operator.
 // See include/bccb_b200.h for the interface and the reference functions replaced.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <climits>
@@ -88,11 +89,19 @@ static void prof_after(ProfEvent* e, cudaStream_t st) {
 extern "C" long long bccb_launch_count(void) { return g_launches.load(); }
 
 // Set at the top of every public entry point that launches kernels (EntryScope); consumed by
-// the first launch_pass of the call.
+// the first launch_pass of the call.  The scope is also an NVTX range named after the entry
+// point (header-only NVTX 3: free unless a profiler is attached), so nsys / ncu timelines
+// group each call's kernels.
 static thread_local bool t_entry_fresh = false;
 struct EntryScope {
-  EntryScope() { t_entry_fresh = true; }
-  ~EntryScope() { t_entry_fresh = false; }
+  explicit EntryScope(const char* name) {
+    t_entry_fresh = true;
+    nvtxRangePushA(name);
+  }
+  ~EntryScope() {
+    t_entry_fresh = false;
+    nvtxRangePop();
+  }
 };
 
 extern "C" int bccb_profile_begin(void) {
@@ -524,9 +533,7 @@ static bool rows_use_kp16(const AxisHost& ax) { return rows_kp16_env() && kp16_s
 // Shapes with an instantiation: (KP, Mo) at R = 128.
 #define TC_SHAPES(X)                                       \
   X(32, 4)   /* L1 = 4096, band 128 (config 5) */          \
-  X(8, 8)    /* L1 = 1024, band 64  (config 4) */          \
-  X(16, 4)   /* L1 = 2048, band 64 */                      \
-  X(16, 8)   /* L1 = 2048, band 128 */
+  X(8, 8)    /* L1 = 1024, band 64  (config 4) */
 static int rows_tc_env() {
   static const int v = [] {
     const char* e = getenv("BCCB_ROWS_TC");
@@ -872,26 +879,30 @@ static FusedCols make_fused(const bccb_plan_s* p, int batch, const Workspace& w,
 
 // Tensor-core rows pass (rows_fista_tc_kernel): persistent CTAs (resident CTAs per SM x SMs),
 // shared memory = band tile + forward transpose + staged twiddles + A tiles + B tiles.
-template <int KP, int MO, bool MOM>
+template <int KP, int MO, bool MOM, bool TRACE>
 static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
                            const EpiFista& epi, unsigned* fl, cudaStream_t st) {
   using TS = TileShape<KP, 128, MO>;
   using TSH = TcShape<KP, MO, TS::TR>;
   // resident CTAs per SM the register budget targets: the KP-point register DFT dominates
   constexpr int MINB = KP == 8 ? 4 : (KP == 16 ? 3 : 2);
-  auto k = rows_fista_tc_kernel<KP, MO, MOM, MINB>;
+  auto k = rows_fista_tc_kernel<KP, MO, MOM, MINB, TRACE>;
   size_t smem = (size_t)(TS::TR * TS::XP + TS::TR * TS::SP) * sizeof(float2);
   if (TS::STAGE_TW) smem += (size_t)(KP + MO) * 128 * sizeof(float2);
   smem = ((smem + 127) & ~(size_t)127) + TSH::A_BYTES + TSH::B_BYTES;
-  static int occ[2] = {0, 0};            // per MOM instantiation: resident CTAs per SM
-  int& o = occ[MOM ? 1 : 0];
+  // resident CTAs per SM: the register budget of __launch_bounds__ (MINB), capped by shared
+  // memory (228 KB per SM, 1 KB reserved per CTA) and TMEM (512 columns per SM).  The shared-
+  // memory carveout is pinned to its maximum so the driver does not pick a smaller split (the
+  // occupancy API's default-carveout answer gave one CTA per SM: profiles/r2/r2b_*).
+  static int o = 0;                      // per instantiation
   if (!o) {
     int rc = prep_smem(k, smem);
     if (rc) return rc;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 256, smem));
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
+    o = std::min<int>(MINB, (int)((228 * 1024) / (smem + 1024)));
+    o = std::min(o, 512 / TSH::COLS);
     if (o < 1) return fail(BCCB_ERR_UNSUPPORTED, "tensor-core rows pass does not fit one SM");
-    // every resident CTA holds TSH::COLS TMEM columns (512 per SM)
-    if (o * TSH::COLS > 512) o = 512 / TSH::COLS;
   }
   const int ntiles = (int)((G.rows + TS::TR - 1) / TS::TR);
   const unsigned grid = (unsigned)std::min<long long>(ntiles, (long long)o * num_sms());
@@ -912,10 +923,14 @@ static int launch_rows_fista_tc(const bccb_plan_s* p, int batch, bool inv, bool 
   const AxisT<float2> ax = p->ax1.dev_t();
   unsigned* fl = (unsigned*)w.flags;
   const bool mom = epi.momentum != 0;
-#define TC_CASE(KP_, MO_)                                                                \
-  if (ax.KP == KP_ && ax.Mo == MO_)                                                      \
-    return mom ? launch_tc_shape<KP_, MO_, true>(p, G, ax, io, epi, fl, st)              \
-               : launch_tc_shape<KP_, MO_, false>(p, G, ax, io, epi, fl, st);
+#define TC_CASE(KP_, MO_)                                                                          \
+  if (ax.KP == KP_ && ax.Mo == MO_) {                                                              \
+    if (epi.trace)                                                                                 \
+      return mom ? launch_tc_shape<KP_, MO_, true, true>(p, G, ax, io, epi, fl, st)                \
+                 : launch_tc_shape<KP_, MO_, false, true>(p, G, ax, io, epi, fl, st);              \
+    return mom ? launch_tc_shape<KP_, MO_, true, false>(p, G, ax, io, epi, fl, st)                 \
+               : launch_tc_shape<KP_, MO_, false, false>(p, G, ax, io, epi, fl, st);               \
+  }
   TC_SHAPES(TC_CASE)
 #undef TC_CASE
   return fail(BCCB_ERR_UNSUPPORTED, "no tensor-core rows specialisation (KP %d, Mo %d)", ax.KP, ax.Mo);
@@ -923,6 +938,7 @@ static int launch_rows_fista_tc(const bccb_plan_s* p, int batch, bool inv, bool 
 
 static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                                   const EpiFista& epi, bool zs, cudaStream_t st, const FusedCols* fused = nullptr) {
+  if (!zs) return fail(BCCB_ERR_UNSUPPORTED, "the specialised rows pass runs with zero-segment skipping");
   LaunchShape sh = fast_shape(p);
   const Geo G = rows_geo(p, batch, sh, inv, fwd);
   RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
@@ -953,27 +969,35 @@ static int launch_rows_fista_fast(const bccb_plan_s* p, int batch, bool inv, boo
     const FusedCols nofc16{};
     const int k16 = fast_key(p->ax1.s);
 #define K16_CASE(R_, MO_)                                                                                \
-  if (k16 == 16 * 100000 + R_ * 10 + MO_)                                                                \
+  if (k16 == 16 * 100000 + R_ * 10 + MO_) {                                                              \
+    if (epi.trace)                                                                                       \
+      return mom ? launch_pass<float2>(rows_fista_fast_kernel<16, R_, MO_, true, true, 0, 3, true>, KIND_ROWS, grid, \
+                                       sh, st, G, axs, io, epi, fl, nofc16)                              \
+                 : launch_pass<float2>(rows_fista_fast_kernel<16, R_, MO_, false, true, 0, 3, true>, KIND_ROWS,    \
+                                       grid, sh, st, G, axs, io, epi, fl, nofc16);                       \
     return mom ? launch_pass<float2>(rows_fista_fast_kernel<16, R_, MO_, true, true, 0, 3>, KIND_ROWS, grid, sh, \
                                      st, G, axs, io, epi, fl, nofc16)                                    \
                : launch_pass<float2>(rows_fista_fast_kernel<16, R_, MO_, false, true, 0, 3>, KIND_ROWS, grid, sh, \
-                                     st, G, axs, io, epi, fl, nofc16);
+                                     st, G, axs, io, epi, fl, nofc16);                                   \
+  }
     K16_CASE(16, 2) K16_CASE(64, 4)
 #undef K16_CASE
   }
   const FusedCols nofc{};
-#define FAST_CASE(KP_, R_, MO_)                                                                              \
-  if (key == KP_ * 100000 + R_ * 10 + MO_) {                                                                 \
-    if (zs)                                                                                                  \
-      return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true>, KIND_ROWS, grid, sh, st, \
-                                       G, ax, io, epi, fl, nofc)                                             \
-                 : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true>, KIND_ROWS, grid, sh,   \
-                                       st, G, ax, io, epi, fl, nofc);                                        \
-    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, false>, KIND_ROWS, grid, sh, st,  \
-                                     G, ax, io, epi, fl, nofc)                                               \
-               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, false>, KIND_ROWS, grid, sh, st, \
-                                     G, ax, io, epi, fl, nofc);                                              \
+  if (epi.trace) {   // traced variants exist for the config-5 line shape only (trace_supported)
+    if (zs && key == 32 * 100000 + 128 * 10 + 4)
+      return mom ? launch_pass<float2>(rows_fista_fast_kernel<32, 128, 4, true, true, 0, 2, true>, KIND_ROWS, grid,
+                                       sh, st, G, ax, io, epi, fl, nofc)
+                 : launch_pass<float2>(rows_fista_fast_kernel<32, 128, 4, false, true, 0, 2, true>, KIND_ROWS, grid,
+                                       sh, st, G, ax, io, epi, fl, nofc);
+    return fail(BCCB_ERR_UNSUPPORTED, "no traced rows specialisation for this line shape");
   }
+#define FAST_CASE(KP_, R_, MO_)                                                                              \
+  if (key == KP_ * 100000 + R_ * 10 + MO_)                                                                   \
+    return mom ? launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, true, true>, KIND_ROWS, grid, sh, st,   \
+                                     G, ax, io, epi, fl, nofc)                                               \
+               : launch_pass<float2>(rows_fista_fast_kernel<KP_, R_, MO_, false, true>, KIND_ROWS, grid, sh, st,  \
+                                     G, ax, io, epi, fl, nofc);
   FAST_SHAPES(FAST_CASE)
 #undef FAST_CASE
   return fail(BCCB_ERR_UNSUPPORTED, "no specialisation for this line shape");
@@ -1246,19 +1270,19 @@ static int matvec_impl(bccb_plan_t p, int batch, const void* x, void* y, void* w
 
 extern "C" int bccb_matvec(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
                            void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_matvec");
   return matvec_impl<float2>(p, batch, x, y, workspace, stream);
 }
 
 extern "C" int bccb_matvec_z(bccb_plan_t p, int batch, const void* x, void* y, void* workspace,
                              void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_matvec_z");
   return matvec_impl<double2>(p, batch, x, y, workspace, stream);
 }
 
 extern "C" int bccb_spectrum_box(bccb_plan_t p, int batch, const void* x, void* out_box,
                                  void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_spectrum_box");
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!x || !out_box) return fail(BCCB_ERR_INVALID, "x / out_box is NULL");
@@ -1273,7 +1297,7 @@ extern "C" int bccb_spectrum_box(bccb_plan_t p, int batch, const void* x, void* 
 extern "C" int bccb_synthesize(bccb_plan_t p, int batch, const void* box, float scale, const void* x,
                                float alpha, void* out, float* maxabs, void* workspace,
                                void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_synthesize");
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!box) return fail(BCCB_ERR_INVALID, "box is NULL");
@@ -1310,7 +1334,7 @@ __global__ void adjoint_scatter_kernel(const float2* __restrict__ y, const int* 
 
 extern "C" int bccb_adjoint(bccb_plan_t p, int batch, const void* y, void* bhat_box, void* b,
                             float* maxabs, void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_adjoint");
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!p->occ_dev || p->M < 1) return fail(BCCB_ERR_INVALID, "bccb_adjoint needs a Gram plan");
@@ -1577,7 +1601,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
                               double mu, const double* tau,
                               const void* bhat_box, const void* extra, void* c, void* d,
                               int* first_bad, void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_fista_run");
   return fista_run_impl(p, batch, first_iteration, iterations, mu, tau, bhat_box, extra, c, d, first_bad,
                         workspace, stream, nullptr);
 }
@@ -1585,7 +1609,7 @@ extern "C" int bccb_fista_run(bccb_plan_t p, int batch, int first_iteration, int
 extern "C" int bccb_fista_run_traced(bccb_plan_t p, int batch, int iterations, double mu, const double* tau,
                                      const void* bhat_box, void* c, void* d, int* first_bad, double* trace,
                                      void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_fista_run_traced");
   if (!trace) return fail(BCCB_ERR_INVALID, "NULL trace");
   return fista_run_impl(p, batch, 0, iterations, mu, tau, bhat_box, nullptr, c, d, first_bad, workspace, stream,
                         trace);
@@ -1632,8 +1656,11 @@ static int fista_run_impl(bccb_plan_t p, int batch, int first_iteration, int ite
   // fused objective trace: the per-pass kernels with zero-segment skipping, a Gram-type
   // spectrum (zero outside the box) and the right-hand side on the box
   if (trace) {
+    // traced rows variants: the tensor-core engine, the KP16 engine and the config-5 KP32 shape
+    const bool traced_shape = rows_use_tc(p->ax1) || rows_use_kp16(p->ax1) ||
+                              fast_key(p->ax1.f) == 32 * 100000 + 128 * 10 + 4;
     if (first_iteration != 0 || extra || p->lam_out != std::complex<double>(0.0, 0.0) ||
-        !fast_supported(p, batch, extra))
+        !fast_supported(p, batch, extra) || !traced_shape)
       return fail(BCCB_ERR_UNSUPPORTED, "fused objective trace needs a Gram operator on a specialised grid");
     CUDA_TRY(cudaMemsetAsync(trace, 0, (size_t)batch * iterations * sizeof(double), st));
   }
@@ -1961,7 +1988,7 @@ extern "C" int bccb_admm_run(bccb_plan_t p, int batch, int first_iteration, int 
                              double rho, const double* tau,
                              const void* bhat_box, const void* extra, void* z, void* v, void* c_last,
                              int* first_bad, void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_admm_run");
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (iterations < 1) return fail(BCCB_ERR_INVALID, "iteration count must be positive");
@@ -2019,7 +2046,7 @@ extern "C" size_t bccb_topk_workspace_bytes(int batch, long long length, int k) 
 
 extern "C" int bccb_topk(int batch, long long length, const void* values, int is_double, int k,
                          int* idx, float* mag, void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_topk");
   if (batch < 1 || length < 1) return fail(BCCB_ERR_INVALID, "empty input");
   if (k < 1 || k > 64) return fail(BCCB_ERR_INVALID, "k must lie in [1, 64]");
   if (k > length) return fail(BCCB_ERR_INVALID, "k exceeds the vector length");
@@ -2056,7 +2083,7 @@ extern "C" int bccb_topk(int batch, long long length, const void* values, int is
 // at rtol 1e-11 by the reference's pkg/tests/test_bccb.py:99-107.
 extern "C" int bccb_spectrum_box_z(bccb_plan_t p, int batch, const void* x, void* out_box, void* workspace,
                                    void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_spectrum_box_z");
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!x || !out_box) return fail(BCCB_ERR_INVALID, "x / out_box is NULL");
@@ -2070,7 +2097,7 @@ extern "C" int bccb_spectrum_box_z(bccb_plan_t p, int batch, const void* x, void
 
 extern "C" int bccb_synthesize_z(bccb_plan_t p, int batch, const void* box, double scale, void* out,
                                  void* workspace, void* stream) {
-  EntryScope entry_scope_;
+  EntryScope entry_scope_("bccb_synthesize_z");
   int rc = check_common(p, batch, workspace);
   if (rc) return rc;
   if (!box || !out) return fail(BCCB_ERR_INVALID, "box / out is NULL");

@@ -775,18 +775,17 @@ struct FistaPolicy {
   float2* dp;
   FistaScalars sc;
   float bn;
-  double* tr;       // fused objective: &trace[b][it] (null: off)
-  double tau_b;
   __device__ __forceinline__ FistaPolicy(const EpiFista& e, long long off, int b) {
     cp = e.c + off;
     dp = MOM ? e.d + off : nullptr;
     sc = FistaScalars{e.kscale * e.tau[b], e.a, e.beta_cur, b, e.it, e.first_bad};
     bn = (float)e.beta_next;
-    tr = e.trace ? e.trace + (long long)b * e.trace_stride + e.it : nullptr;
-    tau_b = e.trace ? e.tau[b] : 0.0;
   }
-  __device__ __forceinline__ double* trace_slot() const { return tr; }
-  __device__ __forceinline__ double l1_term(const S& n) const { return tau_b * hypot(n.c.x, n.c.y); }
+  // fused objective: |c_{t+1}| of an updated point (float: summed over at most KP points per
+  // thread, then in float64 across threads)
+  __device__ __forceinline__ static float l1_term(const S& n) {
+    return sqrtf((float)(n.c.x * n.c.x + n.c.y * n.c.y));
+  }
   __device__ __forceinline__ double kap() const { return sc.kap; }
   __device__ __forceinline__ S load(int o, bool live) const {
     S s;
@@ -900,9 +899,15 @@ struct AdmmSplitPolicy {
   __device__ __forceinline__ float2 first_x(const S& s) const {
     return make_float2((float)(s.z.x - s.r.x), (float)(s.z.y - s.r.y));
   }
-  __device__ __forceinline__ double* trace_slot() const { return nullptr; }
-  __device__ __forceinline__ double l1_term(const S&) const { return 0.0; }
+  __device__ __forceinline__ static float l1_term(const S&) { return 0.f; }
 };
+
+// fused objective trace slot of the rows pass, read from the kernel parameters (constant
+// bank) only where it is used, so the untraced pass keeps its register budget
+__device__ __forceinline__ void trace_add(const EpiFista& e, int b, double v) {
+  atomicAdd(e.trace + (long long)b * e.trace_stride + e.it, e.tau[b] * v);
+}
+__device__ __forceinline__ void trace_add(const EpiAdmmSplit&, int, double) {}
 
 // Tensor-core level 2 of the band inverse (TCI rows tiles, R = 128 threads per line).
 // For each line and register slot j the level-2 sum is
@@ -1042,7 +1047,7 @@ __device__ __forceinline__ void tc_read(TcInv& t, int ii, float2 (&a)[KP]) {
 // state policy Pol.  `tile` indexes the tile (and its flag words); with KP2 > 0 and do_fwd,
 // the last tile of a snapshot to arrive runs that snapshot's column pass.  Streaming state /
 // band loads bypass L1 (ld.global.cg): they are read once.
-template <int KP, int R, int MO, typename Pol, bool ZS, int KP2, bool TCI = false>
+template <int KP, int R, int MO, typename Pol, bool ZS, int KP2, bool TCI = false, bool TRACE = false>
 __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
                                           const typename Pol::Args& epi, unsigned* __restrict__ flags,
                                           const FusedCols& fc, int tile, const float2* tw1s, const float2* tw2s,
@@ -1116,7 +1121,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       if (tid == 0) tc_issue<KP, MO, TR>(*tci);
     }
     unsigned nfl = 0;
-    double l1 = 0.0;          // fused objective: tau_b |c_{t+1}| over this thread's updated points
+    float l1 = 0.f;           // fused objective: sum of |c_{t+1}| over this thread's updated points
     if constexpr (TCI) {
       // ---- band inverse: level 2 on the tensor core (TcInv), twiddle, level-1 register IDFT
       tc_read<KP, MO, TR>(*tci, ii, a);
@@ -1186,7 +1191,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
           if (active && !(Pol::zero(sb[q]) && fmaf(g.x, g.x, g.y * g.y) < kap2_lo)) {
             n = pol.update(sb[q], g);
             if (!ZS) pol.store(r * R, n);
-            if (pol.trace_slot()) l1 += pol.l1_term(n);
+            if constexpr (TRACE) l1 += Pol::l1_term(n);
           }
           if (ZS) {
             if (__any_sync(0xffffffffu, !Pol::zero(n))) {  // segment (still / newly) nonzero: write it whole
@@ -1203,10 +1208,11 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       }
     }
     if (ZS && lane == 0) *fw = nfl;
-    if (pol.trace_slot()) {   // whole CTA in one snapshot: one atomic per warp
+    if constexpr (TRACE) {   // whole CTA in one snapshot: one atomic per warp
+      double v = (double)l1;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-      if (lane == 0 && l1 != 0.0) atomicAdd(pol.trace_slot(), l1);
+      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && v != 0.0) trace_add(epi, b, v);
     }
   } else if (active) {
 #pragma unroll
@@ -1292,7 +1298,9 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   }
 }
 
-template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0, int MINB = 2>
+// TRACE: the fused objective trace variant (tau ||c||_1 summed over the updated points);
+// a separate instantiation so the plain pass keeps its register budget.
+template <int KP, int R, int MO, bool MOM, bool ZS, int KP2 = 0, int MINB = 2, bool TRACE = false>
 __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
     rows_fista_fast_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
                            FusedCols fc) {
@@ -1302,14 +1310,15 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
   const float2* tw1s;
   const float2* tw2s;
   stage_twiddles<KP, R, MO>(ax, Xs + TS::TR * TS::XP + TS::TR * TS::SP, tw1s, tw2s);
-  rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s, Xs);
+  rows_tile<KP, R, MO, FistaPolicy<MOM>, ZS, KP2, false, TRACE>(G, ax, io, epi, flags, fc, blockIdx.x, tw1s, tw2s,
+                                                               Xs);
 }
 
 // Tensor-core variant of the specialised FISTA/ISTA rows pass (lines of L1 = 128 KP points, band
 // K = KP MO): the level-2 stage of the band inverse runs as kind::tf32 MMAs (TcInv), the rest
 // of rows_tile is unchanged.  Persistent: each CTA stages the constant A tiles, allocates its
 // TMEM columns and initialises its mbarrier once, then walks tiles blockIdx.x, +gridDim.x, ...
-template <int KP, int MO, bool MOM, int MINB>
+template <int KP, int MO, bool MOM, int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB)
     rows_fista_tc_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
                          int ntiles) {
@@ -1344,7 +1353,8 @@ __global__ void __launch_bounds__(256, MINB)
   t.tmem = tmem_base;
   const FusedCols nofc{};
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs, &t);
+    rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true, TRACE>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs,
+                                                                 &t);
     __syncthreads();   // Xs / S / B tiles and TMEM are reused by the next tile
   }
   tc::fence_before_sync();
