@@ -404,8 +404,6 @@ def main():
     launches0 = _lib.lib.bccb_launch_count()
     ms_k = (ctypes.c_double * 3)()
     n_k = (ctypes.c_longlong * 3)()
-    if not args.no_kernel_events:
-        _lib.lib.bccb_profile_begin()
     for _ in range(args.steps):
         reset()
         barrier()
@@ -418,8 +416,6 @@ def main():
         barrier()
         times.append(e0.elapsed_time(e1))
     launches = _lib.lib.bccb_launch_count() - launches0
-    if not args.no_kernel_events:
-        _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
     clk = clocks.stop()
     ms_local = statistics.mean(times)
     ms_step = bdist.max_over_ranks(ms_local)
@@ -427,20 +423,36 @@ def main():
     value = total * L * T / (ms_step / 1e3)
     nsub = int(_lib.lib.bccb_substreams_for(op._plan, B))
 
+    # ---- per-launch kernel timing: one more step in the SAME stream configuration with every
+    # library launch bracketed by CUDA events on its own stream (events between the passes cost
+    # PDL overlap at short lines, so they stay out of the timed steps; at config 5 they were
+    # measured neutral: profiles/r2/r2a_bench_cfg5_noev.json)
     roofline = None
-    if not args.no_kernel_events and n_k[0]:
-        K = args.steps
-        rows_ms = ms_k[0] / n_k[0]
-        cols = None
-        if n_k[1]:
-            cols_ms = ms_k[1] / n_k[1]
-            cols = {"kernel": "cols pass (band FFT . D + P.Bhat . band IFFT)", "avg_launch_ms": cols_ms,
-                    "launches_per_step": n_k[1] // K, "share_of_step": ms_k[1] / (K * ms_local)}
-        roofline = build_roofline(w, T, B, value / world, rows_ms, n_k[0] // K, ms_k[0] / K, ms_local, cols, clk)
-        roofline["substreams"] = nsub
-        if nsub > 1:
-            roofline["launch_timing"] += (f"; {nsub} sub-batch streams run concurrently, so per-launch "
-                                          "durations include time shared with the other streams")
+    if not args.no_kernel_events:
+        reset()
+        torch.cuda.synchronize(dev)
+        pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _lib.lib.bccb_profile_begin()
+        pe0.record(stream)
+        run()
+        pe1.record(stream)
+        _lib.check(_lib.lib.bccb_profile_end(ms_k, n_k))
+        torch.cuda.synchronize(dev)
+        prof_ms = pe0.elapsed_time(pe1)
+        if n_k[0]:
+            rows_ms = ms_k[0] / n_k[0]
+            cols = None
+            if n_k[1]:
+                cols = {"kernel": "cols pass (band FFT . D + P.Bhat . band IFFT)", "avg_launch_ms": ms_k[1] / n_k[1],
+                        "launches_per_step": n_k[1], "share_of_step": ms_k[1] / prof_ms}
+            roofline = build_roofline(w, T, B, value / world, rows_ms, n_k[0], ms_k[0], prof_ms, cols, clk)
+            roofline["substreams"] = nsub
+            roofline["profiled_step_ms"] = prof_ms
+            roofline["launch_timing"] = ("CUDA events around every launch of one extra step (same stream "
+                                         "configuration as the timed steps), on the launch's stream")
+            if nsub > 1:
+                roofline["launch_timing"] += (f"; {nsub} sub-batch streams run concurrently, so per-launch "
+                                              "durations include time shared with the other streams")
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None

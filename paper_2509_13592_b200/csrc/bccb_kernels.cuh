@@ -933,7 +933,12 @@ struct TcShape {
   static constexpr int QS = MO / 4;                 // K steps of 8 tf32
   static constexpr int A_BYTES = QS * 4 * 128 * 32;
   static constexpr int B_BYTES = QS * 2 * N * 32;
-  static constexpr int COLS = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : (2 * N <= 256 ? 256 : 512)));
+  // TMEM columns: D_re [0, N), D_im [N, 2N), then the level-1 twiddles conj(w_N^{s j}) of lane s
+  // (re [2N, 2N + KP), im [2N + KP, 2N + 2KP)): resident for the CTA's lifetime, read with
+  // tcgen05.ld instead of KP global/L1 loads per line
+  static constexpr int TW = 2 * N;
+  static constexpr int USED = 2 * N + 2 * KP;
+  static constexpr int COLS = USED <= 32 ? 32 : (USED <= 64 ? 64 : (USED <= 128 ? 128 : (USED <= 256 ? 256 : 512)));
   static_assert(MO % 4 == 0 && MO <= 16, "tensor-core band: MO must be 4, 8, 12 or 16");
   static_assert(N % 16 == 0 && N <= 256, "tensor-core band: N = KP * TR must be a multiple of 16, <= 256");
 };
@@ -1008,37 +1013,65 @@ __device__ __forceinline__ void tc_issue(const TcInv& t) {
   tc::commit(t.mbar);
 }
 
-// thread (ii, s): its KP level-2 values of line ii from TMEM
+// once per CTA: lane s's level-1 twiddles conj(w_N^{s j}), j < KP, into TMEM (warps of the
+// first line team; the second team reads the same lanes)
+template <int KP, int MO, int TR>
+__device__ __forceinline__ void tc_put_twiddles(const TcInv& t, const float2* tw1, int R) {
+  using TSH = TcShape<KP, MO, TR>;
+  if (threadIdx.x >= 128) return;
+  const int s = threadIdx.x;
+  const uint32_t base = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16) + TSH::TW;
+#pragma unroll
+  for (int q = 0; q < KP / 8; ++q) {
+    float re[8], im[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float2 w = __ldg(tw1 + (8 * q + i) * R + s);
+      re[i] = w.x;
+      im[i] = -w.y;                       // conjugate: the inverse transform
+    }
+    tc::tmem_st8(base + 8 * q, re);
+    tc::tmem_st8(base + KP + 8 * q, im);
+  }
+  tc::tmem_st_wait();
+}
+
+// forward level-1 twiddle from the TMEM copy: a[j] *= w_N^{s j} (the stored value is its conjugate)
+template <int KP, int MO, int TR>
+__device__ __forceinline__ void tc_twiddle_fwd(const TcInv& t, float2 (&a)[KP]) {
+  using TSH = TcShape<KP, MO, TR>;
+  const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
+#pragma unroll
+  for (int q = 0; q < KP / 8; ++q) {
+    float wr[8], wi[8];
+    tc::tmem_ld8(lane + TSH::TW + 8 * q, wr);
+    tc::tmem_ld8(lane + TSH::TW + KP + 8 * q, wi);
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[8 * q + i] = cmulc(a[8 * q + i], make_float2(wr[i], wi[i]));
+  }
+}
+
+// thread (ii, s): its KP level-2 values of line ii from TMEM, times the level-1 twiddles
 template <int KP, int MO, int TR>
 __device__ __forceinline__ void tc_read(TcInv& t, int ii, float2 (&a)[KP]) {
   using TSH = TcShape<KP, MO, TR>;
+  static_assert(KP % 8 == 0, "tensor-core band: KP 8, 16 or 32");
   tc::mbar_wait(t.mbar, t.phase);
   t.phase ^= 1u;
   tc::fence_after_sync();
-  const uint32_t lane_base = (uint32_t)((threadIdx.x >> 5) & 3) * 32u;
-  const uint32_t col = t.tmem + (lane_base << 16) + (uint32_t)(ii * KP);
-  if constexpr (KP == 32) {
-    float re[32], im[32];
-    tc::tmem_ld32(col, re);
-    tc::tmem_ld32(col + TSH::N, im);
+  const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
+  const uint32_t col = lane + (uint32_t)(ii * KP);
+#pragma unroll
+  for (int q = 0; q < KP / 8; ++q) {      // quarters of 8 slots: 32 live temporaries
+    float re[8], im[8], wr[8], wi[8];
+    tc::tmem_ld8(col + 8 * q, re);
+    tc::tmem_ld8(col + TSH::N + 8 * q, im);
+    tc::tmem_ld8(lane + TSH::TW + 8 * q, wr);
+    tc::tmem_ld8(lane + TSH::TW + KP + 8 * q, wi);
     tc::tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < KP; ++j) a[j] = make_float2(re[j], im[j]);
-  } else if constexpr (KP == 16) {
-    float re[16], im[16];
-    tc::tmem_ld16(col, re);
-    tc::tmem_ld16(col + TSH::N, im);
-    tc::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < KP; ++j) a[j] = make_float2(re[j], im[j]);
-  } else {
-    static_assert(KP == 8, "tensor-core band: KP 8, 16 or 32");
-    float re[8], im[8];
-    tc::tmem_ld8(col, re);
-    tc::tmem_ld8(col + TSH::N, im);
-    tc::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < KP; ++j) a[j] = make_float2(re[j], im[j]);
+    for (int i = 0; i < 8; ++i) a[8 * q + i] = cmul(make_float2(re[i], im[i]), make_float2(wr[i], wi[i]));
   }
   tc::fence_before_sync();   // these TMEM reads precede the next tile's MMAs (barrier between)
 }
@@ -1124,9 +1157,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     float l1 = 0.f;           // fused objective: sum of |c_{t+1}| over this thread's updated points
     if constexpr (TCI) {
       // ---- band inverse: level 2 on the tensor core (TcInv), twiddle, level-1 register IDFT
-      tc_read<KP, MO, TR>(*tci, ii, a);
-#pragma unroll
-      for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
+      tc_read<KP, MO, TR>(*tci, ii, a);     // level 2 and the level-1 twiddle
       reg_dft<KP, true>(a);
     }
     {
@@ -1254,8 +1285,14 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     if (active && my_live) {
       reg_dft<KP, false>(a);
       float2* Srow = S + ii * SP;
+      if constexpr (TCI) {     // warp-uniform branch (a warp lies in one line): TMEM twiddles
+        tc_twiddle_fwd<KP, MO, TR>(*tci, a);
 #pragma unroll
-      for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], tw1s[j * R + s]);
+        for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = a[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = cmul(a[j], tw1s[j * R + s]);
+      }
     }
     __syncthreads();
     for (int idx = tid; idx < TR * K; idx += NT) {
@@ -1351,6 +1388,10 @@ __global__ void __launch_bounds__(256, MINB)
   __syncthreads();
   tc::fence_after_sync();
   t.tmem = tmem_base;
+  tc_put_twiddles<KP, MO, TS::TR>(t, ax.tw1, R);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
   const FusedCols nofc{};
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true, TRACE>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs,
