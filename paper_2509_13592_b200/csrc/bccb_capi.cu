@@ -549,7 +549,13 @@ static bool tc_shape(const AxisPrec& a) {
 #undef TC_KEY
   return false;
 }
-static bool rows_use_tc(const AxisHost& ax) { return rows_tc_env() && tc_shape(ax.t); }
+// 1 (default): the shapes where the tensor-core engine measured faster (KP = 32: config 5,
+// 365 vs 310 G gpi/s; at KP = 8 (config 4) the CUDA-core KP16 engine stays ahead, 296 vs 236,
+// profiles/r2/r2d_*); 2: every TC shape; 0: off
+static bool rows_use_tc(const AxisHost& ax) {
+  const int env = rows_tc_env();
+  return env && tc_shape(ax.t) && (env == 2 || ax.t.KP == 32);
+}
 
 // rows engine of the specialised passes: tc = the FISTA/ISTA tensor-core engine
 static const AxisPrec& rows_axis(const AxisHost& ax, bool tc = false) {
@@ -889,7 +895,7 @@ static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float
   auto k = rows_fista_tc_kernel<KP, MO, MOM, MINB, TRACE>;
   size_t smem = (size_t)(TS::TR * TS::XP + TS::TR * TS::SP) * sizeof(float2);
   if (TS::STAGE_TW) smem += (size_t)(KP + MO) * 128 * sizeof(float2);
-  smem = ((smem + 127) & ~(size_t)127) + TSH::A_BYTES + TSH::B_BYTES;
+  smem = ((smem + 127) & ~(size_t)127) + TSH::A_BYTES + 2 * TSH::B_BYTES;   // B double-buffered
   // resident CTAs per SM: the register budget of __launch_bounds__ (MINB), capped by shared
   // memory (228 KB per SM, 1 KB reserved per CTA) and TMEM (512 columns per SM).  The shared-
   // memory carveout is pinned to its maximum so the driver does not pick a smaller split (the

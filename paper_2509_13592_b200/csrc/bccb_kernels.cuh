@@ -919,12 +919,18 @@ __device__ __forceinline__ void trace_add(const EpiAdmmSplit&, int, double) {}
 // split into tf32 hi + lo and the product taken as A_hi B_hi + A_lo B_hi + A_hi B_lo (3 MMAs),
 // fp32-grade (tests/test_gpu_tc.py).  D_re sits in TMEM columns [0, N), D_im in [N, 2N),
 // N = TR KP; TMEM lane s belongs to thread s of each line team (warp w reads lanes 32 (w % 4)..).
+// Software pipeline across the persistent CTA's tiles: while tile i is computed, the MMA of
+// tile i (issued during tile i-1) has finished and tile i+1's band sits in the other B buffer
+// with its MMA in flight.  D (TMEM) is single-buffered: every thread reads tile i's D before the
+// barrier after which tile i+1's MMA is issued.
 struct TcInv {
   unsigned char* At;   // [MO/4][re_hi | re_lo | im_hi | im_lo][128 x 8 tf32] (K-major, 4 KB each)
-  unsigned char* Bt;   // [MO/4][hi | lo][N x 8 tf32]
+  unsigned char* Bt[2];// double-buffered [MO/4][hi | lo][N x 8 tf32]
   uint64_t* mbar;      // MMA completion (tcgen05.commit)
   uint32_t tmem;       // TMEM base column (lane 0)
   uint32_t phase;      // mbarrier parity of the next completion
+  int buf;             // B buffer of the tile being computed
+  int next;            // next tile of this CTA (-1: none)
 };
 
 template <int KP, int MO, int TR>
@@ -989,14 +995,14 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bt, int k, int i2, float
 
 // one elected thread: the tile's 6 * MO/4 MMAs, then commit to the mbarrier
 template <int KP, int MO, int TR>
-__device__ __forceinline__ void tc_issue(const TcInv& t) {
+__device__ __forceinline__ void tc_issue(const TcInv& t, const unsigned char* Bt) {
   using TSH = TcShape<KP, MO, TR>;
   constexpr uint32_t idesc = tc::idesc_tf32<128, TSH::N>();
   tc::fence_after_sync();
 #pragma unroll
   for (int q = 0; q < TSH::QS; ++q) {
     const unsigned char* a = t.At + q * 4 * 4096;
-    const unsigned char* b = t.Bt + q * 2 * TSH::N * 32;
+    const unsigned char* b = Bt + q * 2 * TSH::N * 32;
     const uint64_t are_hi = tc::desc_kmajor(a, tc::KM_LBO, tc::KM_SBO);
     const uint64_t are_lo = tc::desc_kmajor(a + 4096, tc::KM_LBO, tc::KM_SBO);
     const uint64_t aim_hi = tc::desc_kmajor(a + 2 * 4096, tc::KM_LBO, tc::KM_SBO);
@@ -1136,30 +1142,44 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   }
   if constexpr (PRE_WAIT_READS) pdl_wait();
   if (G.do_inv) {
-    // band tile V[b][k][l20 + ii] -> Xs[ii][k]   (TCI: -> the MMA's B tiles, tf32 hi/lo)
-    for (int idx = tid; idx < TR * K; idx += NT) {
-      const int k = idx / TR, i2 = idx % TR;
-      const float2 v = __ldcg(io.V + vbase + (long long)k * L2 + i2);
-      if constexpr (TCI) tc_put_b<KP, MO, TR>(tci->Bt, k, i2, v);
-      else Xs[i2 * XP + k] = v;
+    if constexpr (TCI) {
+      // pipelined tensor-core level 2: this tile's MMA is in flight (issued during the previous
+      // tile); stage the NEXT tile's band V[b'][k][l2' + i] into the other B buffer (tf32 hi/lo)
+      if (tci->next >= 0) {
+        const int nrow0 = tci->next * TR;
+        const int nb = nrow0 / L2;
+        const long long nvbase = (long long)nb * K * L2 + (nrow0 - nb * L2);
+        for (int idx = tid; idx < TR * K; idx += NT) {
+          const int k = idx / TR, i2 = idx % TR;
+          tc_put_b<KP, MO, TR>(tci->Bt[tci->buf ^ 1], k, i2, __ldcg(io.V + nvbase + (long long)k * L2 + i2));
+        }
+      }
+    } else {
+      // band tile V[b][k][l20 + ii] -> Xs[ii][k]
+      for (int idx = tid; idx < TR * K; idx += NT) {
+        const int k = idx / TR, i2 = idx % TR;
+        Xs[i2 * XP + k] = __ldcg(io.V + vbase + (long long)k * L2 + i2);
+      }
     }
     if (!EARLY) {
 #pragma unroll
       for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
     }
     if (G.do_fwd && tid < (TR + 31) / 32) live_rows_zero(tid);
-    if constexpr (TCI) tc::fence_async_smem();   // B tiles -> visible to the tensor core
+    if constexpr (TCI) {
+      // ---- band inverse, level 2 of this tile from TMEM (times the level-1 twiddle); every
+      // thread's D reads and B writes precede the barrier, after which the next MMA is issued
+      tc_read<KP, MO, TR>(*tci, ii, a);
+      tc::fence_async_smem();   // B writes -> visible to the tensor core
+    }
     __syncthreads();
     if constexpr (TCI) {
-      if (tid == 0) tc_issue<KP, MO, TR>(*tci);
+      if (tid == 0 && tci->next >= 0) tc_issue<KP, MO, TR>(*tci, tci->Bt[tci->buf ^ 1]);
+      tci->buf ^= 1;
     }
     unsigned nfl = 0;
     float l1 = 0.f;           // fused objective: sum of |c_{t+1}| over this thread's updated points
-    if constexpr (TCI) {
-      // ---- band inverse: level 2 on the tensor core (TcInv), twiddle, level-1 register IDFT
-      tc_read<KP, MO, TR>(*tci, ii, a);     // level 2 and the level-1 twiddle
-      reg_dft<KP, true>(a);
-    }
+    if constexpr (TCI) reg_dft<KP, true>(a);   // level-1 register IDFT
     {
       // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT); the band row
       // is read as 16-byte pairs
@@ -1374,9 +1394,11 @@ __global__ void __launch_bounds__(256, MINB)
   __shared__ uint32_t tmem_base;
   TcInv t;
   t.At = smem_raw + off;
-  t.Bt = t.At + TSH::A_BYTES;
+  t.Bt[0] = t.At + TSH::A_BYTES;
+  t.Bt[1] = t.Bt[0] + TSH::B_BYTES;
   t.mbar = &mbar;
   t.phase = 0;
+  t.buf = 0;
   tc_stage_a<MO>(t.At, threadIdx.x, TS::NT);
   if (threadIdx.x == 0) {
     tc::mbar_init(&mbar, 1);
@@ -1393,10 +1415,25 @@ __global__ void __launch_bounds__(256, MINB)
   __syncthreads();
   tc::fence_after_sync();
   const FusedCols nofc{};
+  if (G.do_inv && (int)blockIdx.x < ntiles) {
+    // pipeline prologue: the first tile's band -> B[0], its MMA in flight
+    pdl_wait();
+    const int row0 = blockIdx.x * TS::TR;
+    const int b = row0 / G.L2;
+    const long long vbase = (long long)b * TS::K * G.L2 + (row0 - b * G.L2);
+    for (int idx = threadIdx.x; idx < TS::TR * TS::K; idx += TS::NT) {
+      const int k = idx / TS::TR, i2 = idx % TS::TR;
+      tc_put_b<KP, MO, TS::TR>(t.Bt[0], k, i2, __ldcg(io.V + vbase + (long long)k * G.L2 + i2));
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) tc_issue<KP, MO, TS::TR>(t, t.Bt[0]);
+  }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    t.next = tile + (int)gridDim.x < ntiles ? tile + (int)gridDim.x : -1;
     rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true, TRACE>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs,
                                                                  &t);
-    __syncthreads();   // Xs / S / B tiles and TMEM are reused by the next tile
+    __syncthreads();   // Xs / S are reused by the next tile
   }
   tc::fence_before_sync();
   __syncthreads();
