@@ -2067,7 +2067,7 @@ extern "C" int bccb_topk(int batch, long long length, const void* values, int is
     g_launches.fetch_add(2, std::memory_order_relaxed);                                          \
     topk_partial_kernel<KT><<<dim3(nchunk, batch), 256, 0, st>>>(values, is_double, length, k,   \
                                                                  nchunk, cand);                  \
-    topk_merge_kernel<KT><<<batch, 256, 0, st>>>(cand, nchunk * k, k, idx, mag);                 \
+    topk_merge_kernel<<<batch, 256, 0, st>>>(cand, nchunk * k, k, idx, mag);                     \
     break;
   switch (kt) {
     TOPK_CASE(4)

@@ -118,22 +118,39 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const void* __restric
   topk_block_merge<KT>(lst, k, cand + ((long long)b * nchunk + ch) * k);
 }
 
-template <int KT>
+// Phase 2: one CTA per snapshot; k rounds, each a block-wide argmax over the candidates
+// strictly below the previous winner (keys are unique: the index is part of the key).  No
+// per-thread lists: the candidate set (chunks x k) is re-scanned each round.
 __global__ void __launch_bounds__(256) topk_merge_kernel(const TKey* __restrict__ cand, int ncand, int k,
                                                          int* __restrict__ idx, float* __restrict__ mag) {
-  __shared__ TKey res[64];
+  __shared__ TKey warp_best[32];
+  __shared__ TKey best;
   const int b = blockIdx.x;
-  TKey lst[KT];
-#pragma unroll
-  for (int i = 0; i < KT; ++i) lst[i] = key_zero();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   const TKey* c = cand + (long long)b * ncand;
-  for (int i = threadIdx.x; i < ncand; i += blockDim.x) topk_insert<KT>(lst, c[i]);
-  topk_block_merge<KT>(lst, k, res);
-  __syncthreads();
-  for (int r = threadIdx.x; r < k; r += blockDim.x) {
-    const TKey key = res[r];
-    idx[(long long)b * k + r] = (int)(0xFFFFFFFFu - key.b);
-    if (mag) mag[(long long)b * k + r] = (float)__longlong_as_double((long long)key.a);
+  TKey bound{~0ull, ~0u};                 // exclusive upper bound (above every finite key)
+  for (int r = 0; r < k; ++r) {
+    TKey v = key_zero();
+    for (int i = threadIdx.x; i < ncand; i += blockDim.x) {
+      const TKey x = c[i];
+      if (key_gt(bound, x) && key_gt(x, v)) v = x;
+    }
+    v = warp_max_key(v);
+    if (lane == 0) warp_best[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      TKey u = lane < nw ? warp_best[lane] : key_zero();
+      u = warp_max_key(u);
+      if (lane == 0) best = u;
+    }
+    __syncthreads();
+    const TKey w = best;
+    if (threadIdx.x == 0) {
+      idx[(long long)b * k + r] = (int)(0xFFFFFFFFu - w.b);
+      if (mag) mag[(long long)b * k + r] = (float)__longlong_as_double((long long)w.a);
+    }
+    bound = w;
+    __syncthreads();
   }
 }
 
