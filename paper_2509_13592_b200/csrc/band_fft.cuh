@@ -149,33 +149,44 @@ __device__ __forceinline__ void band_fwd_scatter(const C (&A)[KP], int s, const 
   }
 }
 
-// Level-2 forward, part 2: band output o = j + KP*m of a line from its S buffer.
+// Level-2 forward, part 2: band output o = j + KP*m of a line from its S buffer, summed over
+// the thread range s in [s0, s1) (the whole line: 0, R).  Four independent accumulators keep
+// the dependent-add chain at a quarter of the range.
 template <typename C>
-__device__ __forceinline__ C band_fwd_output(const C* __restrict__ S, int o, int KP, const AxisT<C>& ax) {
+__device__ __forceinline__ C band_fwd_partial(const C* __restrict__ S, int o, int KP, const AxisT<C>& ax, int s0,
+                                              int s1) {
   const int j = o % KP;
   const int m = o / KP;
   const C* row = S + j * ax.pitch;
-  C acc0 = cmake(decltype(C::x)(0), decltype(C::x)(0)), acc1 = acc0;
-  const int R = ax.R;
+  const C zero = cmake(decltype(C::x)(0), decltype(C::x)(0));
+  C acc0 = zero, acc1 = zero, acc2 = zero, acc3 = zero;
+  int s = s0;
   if (m == 0) {
-    int s = 0;
-#pragma unroll 4
-    for (; s + 1 < R; s += 2) {
+#pragma unroll 2
+    for (; s + 3 < s1; s += 4) {
       acc0 = cadd(acc0, row[s]);
       acc1 = cadd(acc1, row[s + 1]);
+      acc2 = cadd(acc2, row[s + 2]);
+      acc3 = cadd(acc3, row[s + 3]);
     }
-    if (s < R) acc0 = cadd(acc0, row[s]);
+    for (; s < s1; ++s) acc0 = cadd(acc0, row[s]);
   } else {
-    const C* tw = ax.tw2 + m * R;
-    int s = 0;
-#pragma unroll 4
-    for (; s + 1 < R; s += 2) {
+    const C* tw = ax.tw2 + m * ax.R;
+#pragma unroll 2
+    for (; s + 3 < s1; s += 4) {
       acc0 = cfma(row[s], __ldg(tw + s), acc0);
       acc1 = cfma(row[s + 1], __ldg(tw + s + 1), acc1);
+      acc2 = cfma(row[s + 2], __ldg(tw + s + 2), acc2);
+      acc3 = cfma(row[s + 3], __ldg(tw + s + 3), acc3);
     }
-    if (s < R) acc0 = cfma(row[s], __ldg(tw + s), acc0);
+    for (; s < s1; ++s) acc0 = cfma(row[s], __ldg(tw + s), acc0);
   }
-  return cadd(acc0, acc1);
+  return cadd(cadd(acc0, acc1), cadd(acc2, acc3));
+}
+
+template <typename C>
+__device__ __forceinline__ C band_fwd_output(const C* __restrict__ S, int o, int KP, const AxisT<C>& ax) {
+  return band_fwd_partial(S, o, KP, ax, 0, ax.R);
 }
 
 // Level-2 inverse + level-1 inverse DFT: thread s of a line team turns the K band

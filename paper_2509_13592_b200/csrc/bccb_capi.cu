@@ -1196,14 +1196,19 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   io.K1 = p->ax1.K;
   if (ob) io.ob = *ob;
   const unsigned grid = (unsigned)((G.rows + sh.TR - 1) / sh.TR);
+  // room for the split level-2 forward sums of cols_kernel ([NP][TR*K], NP <= 4) when a CTA
+  // has at least twice as many threads as band outputs
+  LaunchShape shs = sh;
+  if (fwd && sh.threads >= 2 * sh.TR * p->ax2.K)
+    shs.smem += (size_t)std::min(4, sh.threads / (sh.TR * p->ax2.K)) * sh.TR * p->ax2.K * sizeof(C);
   if constexpr (std::is_same<C, float2>::value) {
     const AxisT<C> ax = p->ax2.dev_s(narrow);
     const AxisPrec& ap = narrow ? p->ax2.s8 : p->ax2.s;
     if (cols_warp_supported(p, ap)) return launch_cols_warp<BandMulAdd>(p, ap, G, st, ax, io, BandMulAdd{});
-    KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
+    KP_DISPATCH_F(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, shs, st, G, ax, io));
   } else {
     const AxisT<C> ax = p->ax2.dev<C>();
-    KP_DISPATCH_D(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, sh, st, G, ax, io));
+    KP_DISPATCH_D(ax.KP, return launch_pass<C>(cols_kernel<KPC, C>, KIND_COLS, grid, shs, st, G, ax, io));
   }
   return BCCB_OK;
 }

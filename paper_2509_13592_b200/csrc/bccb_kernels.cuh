@@ -341,7 +341,7 @@ __device__ __forceinline__ ColsPre<C> cols_prefetch(const Geo& G, const AxisT<C>
 template <int KP, typename C, bool U_GLOBAL = true, typename Op = BandMulAdd>
 __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, const ColsIO<C>& io, long long row0,
                                            int TR, C* smem, const Op& op = Op{},
-                                           const ColsPre<C>& pre = ColsPre<C>{}) {
+                                           const ColsPre<C>& pre = ColsPre<C>{}, C* part = nullptr) {
   const int R = ax.R, K = ax.K, N = ax.N;
   const int XP = K + 1, SP = KP * ax.pitch;
   const int nthr = TR * R;
@@ -362,6 +362,25 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     }
     __syncthreads();
   }
+  // Split level-2 forward sums (long lines, few outputs per thread: config 5's column pass has
+  // TR*K = 128 outputs of R = 256 terms for 256 threads): NP threads share each output's
+  // range of s, the partial sums meet in `part` ([NP][TR*K]) and are added in the band loop.
+  const int n_out = TR * K;
+  const int NP = (part && G.do_fwd) ? min(4, (int)blockDim.x / n_out) : 1;
+  if (NP > 1) {
+    for (int idx = tid; idx < NP * n_out; idx += blockDim.x) {
+      const int q = idx / n_out, oi = idx - q * n_out;
+      const int i2 = oi / K, o = oi - i2 * K;
+      part[idx] = band_fwd_partial(S + i2 * SP, o, KP, ax, (q * R) / NP, ((q + 1) * R) / NP);
+    }
+    __syncthreads();
+  }
+  auto fwd_value = [&](int i2, int o) {
+    if (NP == 1) return band_fwd_output(S + i2 * SP, o, KP, ax);
+    C v = part[i2 * K + o];
+    for (int q = 1; q < NP; ++q) v = cadd(v, part[q * n_out + i2 * K + o]);
+    return v;
+  };
   // band values: Y = D*X + P*Bh   (+ the objective's box terms of X when io.ob.chat is set)
   constexpr bool OBJ = std::is_same<C, float2>::value && std::is_same<Op, BandMulAdd>::value;
   long long ob_b = -1;       // snapshot of the running objective sum
@@ -372,7 +391,7 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
     if (g2 >= G.rows) continue;
     C y = cmake(decltype(C::x)(0), decltype(C::x)(0));
     if constexpr (std::is_same<Op, BandMulAdd>::value) {
-      if (G.do_fwd) y = band_fwd_output(S + i2 * SP, o, KP, ax);
+      if (G.do_fwd) y = fwd_value(i2, o);
       if constexpr (OBJ) {
         if (G.do_fwd && io.ob.chat) {
           const long long bb = g2 / io.K1;
@@ -397,7 +416,7 @@ __device__ __forceinline__ void cols_block(const Geo& G, const AxisT<C>& ax, con
         y = cadd(y, bh);
       }
     } else {
-      y = op(g2, o, G.do_fwd ? band_fwd_output(S + i2 * SP, o, KP, ax) : y);
+      y = op(g2, o, G.do_fwd ? fwd_value(i2, o) : y);
     }
     Xs[i2 * XP + o] = y;
   }
@@ -428,7 +447,10 @@ __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT
   const long long row0 = (long long)blockIdx.x * G.TR;
   const ColsPre<C> pre = cols_prefetch(G, ax, io, row0, G.TR);
   pdl_wait();
-  cols_block<KP>(G, ax, io, row0, G.TR, reinterpret_cast<C*>(smem_raw), BandMulAdd{}, pre);
+  // split forward sums when the launch reserved room for them (cols_split_smem)
+  C* base = reinterpret_cast<C*>(smem_raw);
+  C* part = ((int)blockDim.x >= 2 * G.TR * ax.K) ? base + G.TR * (ax.K + 1) + G.TR * KP * ax.pitch : nullptr;
+  cols_block<KP>(G, ax, io, row0, G.TR, base, BandMulAdd{}, pre, part);
 }
 
 // Warp-per-line column pass (complex64 streaming axis with R = 32 threads per line and a band
