@@ -1451,11 +1451,14 @@ __global__ void __launch_bounds__(256, MINB)
     __syncthreads();
     if (threadIdx.x == 0) tc_issue<KP, MO, TS::TR>(t, t.Bt[0]);
   }
+  // No barrier between tiles: the next tile writes shared memory only after barriers every
+  // thread passes after its last read of it here (B is double-buffered; live_rows, Xs and S
+  // are last read before this tile's final __syncthreads), and its MMA overwrites D only after
+  // the barrier that follows every thread's TMEM read.
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     t.next = tile + (int)gridDim.x < ntiles ? tile + (int)gridDim.x : -1;
     rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true, TRACE>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs,
                                                                  &t);
-    __syncthreads();   // Xs / S are reused by the next tile
   }
   tc::fence_before_sync();
   __syncthreads();
