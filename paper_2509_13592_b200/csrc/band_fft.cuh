@@ -124,6 +124,79 @@ __device__ __forceinline__ void reg_dft(C (&a)[P]) {
   }
 }
 
+// Screened inverse register DFT (complex64, P = 16 or 32): a radix-4 decimation-in-frequency
+// first stage splits the P outputs into four residue classes r = 4p + q, each the (P/4)-point
+// inverse DFT of u_q[l] = W_P^{+ql} * sum_i a[(P/4) i + l] (+i)^{qi}.  Parseval bounds every
+// output of class q: |x[4p + q]|^2 <= (P/4) * sum_l |u_q[l]|^2, so when that energy is below
+// the soft threshold for all 32 lanes of the warp (and the class holds no live state: `live`
+// has a bit per register slot), the class's twiddles, sub-DFT and per-point tests are skipped:
+// its points provably stay exactly zero (the bound carries a 2^-10 margin over the per-point
+// fp32 test `|g|^2 < kap2_lo`, far above fp32 rounding of the skipped stages).  Returns the
+// per-lane mask of slots proven below the threshold (all lanes agree on skipped classes);
+// a[] holds x in natural order for the computed classes and unspecified values for skipped
+// ones.  thr_scale <= 0 disables skipping (same arithmetic, every class computed).
+template <int P>
+__device__ __forceinline__ unsigned reg_idft_screened(float2 (&a)[P], float kap2_lo, float thr_scale, unsigned live,
+                                                      bool active) {
+  static_assert(P == 16 || P == 32, "screened inverse DFT: P = 16 or 32");
+  constexpr int Q = P / 4;
+  float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    const float2 s02 = cadd(a[l], a[2 * Q + l]), d02 = csub(a[l], a[2 * Q + l]);
+    const float2 s13 = cadd(a[Q + l], a[3 * Q + l]), d13 = csub(a[Q + l], a[3 * Q + l]);
+    a[l] = cadd(s02, s13);
+    a[2 * Q + l] = csub(s02, s13);
+    a[Q + l] = make_float2(d02.x - d13.y, d02.y + d13.x);       // d02 + i d13
+    a[3 * Q + l] = make_float2(d02.x + d13.y, d02.y - d13.x);   // d02 - i d13
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e[q] = fmaf(a[q * Q + l].x, a[q * Q + l].x, fmaf(a[q * Q + l].y, a[q * Q + l].y, e[q]));
+  }
+  const float thr = kap2_lo * thr_scale;     // thr_scale = (1 - 2^-10) / Q, or <= 0: never skip
+  unsigned ok = 0u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ok |= ((e[q] < thr) || !active ? 1u : 0u) << q;
+  ok = __reduce_and_sync(0xffffffffu, ok);
+  constexpr unsigned ALL = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
+  unsigned pass = 0u;
+  float2 o[P];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    constexpr unsigned CLS = 0x11111111u;
+    const unsigned gm = (CLS << q) & ALL;
+    float2 v[Q];
+#pragma unroll
+    for (int l = 0; l < Q; ++l) v[l] = a[q * Q + l];
+    if (((ok >> q) & 1u) && !(live & gm)) {
+      pass |= gm;
+    } else {
+#pragma unroll
+      for (int l = 1; l < Q; ++l) {
+        const int t = (q * l * (64 / P)) % 64;   // W_P^{+ql} = conj(root64(t))
+        if (t == 0) {
+        } else if (t == 16) {
+          v[l] = make_float2(-v[l].y, v[l].x);
+        } else if (t == 32) {
+          v[l] = make_float2(-v[l].x, -v[l].y);
+        } else if (t == 48) {
+          v[l] = make_float2(v[l].y, -v[l].x);
+        } else {
+          v[l] = cmulc(v[l], c_roots64[t]);
+        }
+      }
+      reg_dft<Q, true>(v);
+#pragma unroll
+      for (int p = 0; p < Q; ++p)
+        pass |= (fmaf(v[p].x, v[p].x, v[p].y * v[p].y) < kap2_lo ? 1u : 0u) << (4 * p + q);
+    }
+#pragma unroll
+    for (int p = 0; p < Q; ++p) o[4 * p + q] = v[p];
+  }
+#pragma unroll
+  for (int r = 0; r < P; ++r) a[r] = o[r];
+  return pass;
+}
+
 // Runtime geometry of one axis at one precision (built on the host: make_axis).
 template <typename C>
 struct AxisT {

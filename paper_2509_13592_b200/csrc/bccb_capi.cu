@@ -685,8 +685,28 @@ static int prep_smem(KernelT kernel, size_t smem) {
     default: return fail(BCCB_ERR_UNSUPPORTED, "register DFT size %d", KPVAL);  \
   }
 
+// Energy screen of the level-1 inverse DFT in the zero-skipping rows passes (band_fft.cuh
+// reg_idft_screened): bitwise neutral; BCCB_SCREEN=0 computes every residue class.
+static int rows_screen_env() {
+  static const int v = [] {
+    const char* e = getenv("BCCB_SCREEN");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+static int debug_env() {
+  static const int v = [] {
+    const char* e = getenv("BCCB_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static Geo rows_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool inv, bool fwd) {
   Geo G;
+  G.screen = rows_screen_env() ? 1 : 0;
+  G.dbg = debug_env();
   G.L1 = p->L1;
   G.L2 = p->L2;
   G.rows = (long long)batch * p->L2;
@@ -895,7 +915,7 @@ static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float
   auto k = rows_fista_tc_kernel<KP, MO, MOM, MINB, TRACE>;
   size_t smem = (size_t)(TS::TR * TS::XP + TS::TR * TS::SP) * sizeof(float2);
   if (TS::STAGE_TW) smem += (size_t)(KP + MO) * 128 * sizeof(float2);
-  smem = ((smem + 127) & ~(size_t)127) + TSH::A_BYTES + 2 * TSH::B_BYTES;   // B double-buffered
+  smem = ((smem + 127) & ~(size_t)127) + TSH::A_BYTES + TSH::B_BYTES;
   // resident CTAs per SM: the register budget of __launch_bounds__ (MINB), capped by shared
   // memory (228 KB per SM, 1 KB reserved per CTA) and TMEM (512 columns per SM).  The shared-
   // memory carveout is pinned to its maximum so the driver does not pick a smaller split (the
@@ -1186,6 +1206,7 @@ static int launch_cols(const bccb_plan_s* p, int batch, bool fwd, bool inv, cons
   G.TR = sh.TR;
   G.do_fwd = fwd ? 1 : 0;
   G.do_inv = inv ? 1 : 0;
+  G.dbg = debug_env();
   ColsIO<C> io{};
   io.U = (const C*)w.U;
   io.V = (C*)w.V;

@@ -38,6 +38,8 @@ struct Geo {
   long long rows;  // total lines in this launch
   int TR;          // lines per CTA
   int do_inv, do_fwd;
+  int screen = 0;  // rows passes: energy-screened level-1 inverse DFT (BCCB_SCREEN, default on)
+  int dbg = 0;     // BCCB_DEBUG bits: 1 = barrier between tensor-core tiles, 2 = unsplit column sums
 };
 
 // ------------------------------------------------------------------ epilogues
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(KP <= 8 ? 1024 : 256) cols_kernel(Geo G, AxisT
   pdl_wait();
   // split forward sums when the launch reserved room for them (cols_split_smem)
   C* base = reinterpret_cast<C*>(smem_raw);
-  C* part = ((int)blockDim.x >= 2 * G.TR * ax.K) ? base + G.TR * (ax.K + 1) + G.TR * KP * ax.pitch : nullptr;
+  C* part = ((int)blockDim.x >= 2 * G.TR * ax.K && !(G.dbg & 2)) ? base + G.TR * (ax.K + 1) + G.TR * KP * ax.pitch : nullptr;
   cols_block<KP>(G, ax, io, row0, G.TR, base, BandMulAdd{}, pre, part);
 }
 
@@ -941,18 +943,22 @@ __device__ __forceinline__ void trace_add(const EpiAdmmSplit&, int, double) {}
 // split into tf32 hi + lo and the product taken as A_hi B_hi + A_lo B_hi + A_hi B_lo (3 MMAs),
 // fp32-grade (tests/test_gpu_tc.py).  D_re sits in TMEM columns [0, N), D_im in [N, 2N),
 // N = TR KP; TMEM lane s belongs to thread s of each line team (warp w reads lanes 32 (w % 4)..).
-// Software pipeline across the persistent CTA's tiles: while tile i is computed, the MMA of
-// tile i (issued during tile i-1) has finished and tile i+1's band sits in the other B buffer
-// with its MMA in flight.  D (TMEM) is single-buffered: every thread reads tile i's D before the
-// barrier after which tile i+1's MMA is issued.
+// Per tile: the band is staged into B (each thread's value was prefetched during the previous
+// tile), one thread issues the MMAs, every thread waits on the mbarrier and reads its lane of D.
+// B and D are single-buffered: the next tile stages B only after every thread has waited for
+// this tile's MMAs, and issues its MMAs after a barrier that follows every thread's D reads.
 struct TcInv {
   unsigned char* At;   // [MO/4][re_hi | re_lo | im_hi | im_lo][128 x 8 tf32] (K-major, 4 KB each)
-  unsigned char* Bt[2];// double-buffered [MO/4][hi | lo][N x 8 tf32]
+  unsigned char* Bt;   // [MO/4][hi | lo][N x 8 tf32]
   uint64_t* mbar;      // MMA completion (tcgen05.commit)
   uint32_t tmem;       // TMEM base column (lane 0)
   uint32_t phase;      // mbarrier parity of the next completion
-  int buf;             // B buffer of the tile being computed
   int next;            // next tile of this CTA (-1: none)
+  // prefetched during the previous tile (pre != 0): this thread's band value of the tile and
+  // the tile's flag words
+  int pre;
+  float2 pv;
+  unsigned pfl, ptw;
 };
 
 template <int KP, int MO, int TR>
@@ -1017,14 +1023,14 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bt, int k, int i2, float
 
 // one elected thread: the tile's 6 * MO/4 MMAs, then commit to the mbarrier
 template <int KP, int MO, int TR>
-__device__ __forceinline__ void tc_issue(const TcInv& t, const unsigned char* Bt) {
+__device__ __forceinline__ void tc_issue(const TcInv& t) {
   using TSH = TcShape<KP, MO, TR>;
   constexpr uint32_t idesc = tc::idesc_tf32<128, TSH::N>();
   tc::fence_after_sync();
 #pragma unroll
   for (int q = 0; q < TSH::QS; ++q) {
     const unsigned char* a = t.At + q * 4 * 4096;
-    const unsigned char* b = Bt + q * 2 * TSH::N * 32;
+    const unsigned char* b = t.Bt + q * 2 * TSH::N * 32;
     const uint64_t are_hi = tc::desc_kmajor(a, tc::KM_LBO, tc::KM_SBO);
     const uint64_t are_lo = tc::desc_kmajor(a + 4096, tc::KM_LBO, tc::KM_SBO);
     const uint64_t aim_hi = tc::desc_kmajor(a + 2 * 4096, tc::KM_LBO, tc::KM_SBO);
@@ -1080,14 +1086,18 @@ __device__ __forceinline__ void tc_twiddle_fwd(const TcInv& t, float2 (&a)[KP]) 
   }
 }
 
-// thread (ii, s): its KP level-2 values of line ii from TMEM, times the level-1 twiddles
-template <int KP, int MO, int TR>
-__device__ __forceinline__ void tc_read(TcInv& t, int ii, float2 (&a)[KP]) {
-  using TSH = TcShape<KP, MO, TR>;
-  static_assert(KP % 8 == 0, "tensor-core band: KP 8, 16 or 32");
+// every thread: wait for the tile's MMAs
+__device__ __forceinline__ void tc_wait(TcInv& t) {
   tc::mbar_wait(t.mbar, t.phase);
   t.phase ^= 1u;
   tc::fence_after_sync();
+}
+
+// thread (ii, s): its KP level-2 values of line ii from TMEM, times the level-1 twiddles
+template <int KP, int MO, int TR>
+__device__ __forceinline__ void tc_read(const TcInv& t, int ii, float2 (&a)[KP]) {
+  using TSH = TcShape<KP, MO, TR>;
+  static_assert(KP % 8 == 0, "tensor-core band: KP 8, 16 or 32");
   const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
   const uint32_t col = lane + (uint32_t)(ii * KP);
 #pragma unroll
@@ -1101,7 +1111,53 @@ __device__ __forceinline__ void tc_read(TcInv& t, int ii, float2 (&a)[KP]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) a[8 * q + i] = cmul(make_float2(re[i], im[i]), make_float2(wr[i], wi[i]));
   }
-  tc::fence_before_sync();   // these TMEM reads precede the next tile's MMAs (barrier between)
+}
+
+// Energy screen straight from TMEM (KP = 32; the thread's state is known to be all zero): the
+// radix-4 first stage of the screened inverse DFT (band_fft.cuh reg_idft_screened) on the
+// level-2 values Z[8 i + l], i < 4, without keeping any of them.  Only the energy of each residue
+// class matters and the level-1 twiddle factors as tw[8 i + l] = tw[8 i] tw[l] with |tw[l]| = 1, so
+// the class sums are formed from Z[8 i + l] tw[8 i] (three per-thread constants read from the TMEM
+// twiddle table).  Returns true when all four class bounds of every lane of the warp lie below
+// the threshold: none of the warp's points can leave zero, and nothing else of the tile's
+// inverse transform is needed.
+template <int KP, int MO, int TR>
+__device__ __forceinline__ bool tc_energy_screen(const TcInv& t, int ii, float thr, bool active) {
+  using TSH = TcShape<KP, MO, TR>;
+  static_assert(KP == 32, "TMEM energy screen: KP = 32");
+  const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
+  const uint32_t col = lane + (uint32_t)(ii * KP);
+  float2 w[3];
+#pragma unroll
+  for (int i = 1; i < 4; ++i)
+    w[i - 1] = make_float2(tc::tmem_ld1(lane + TSH::TW + 8 * i), tc::tmem_ld1(lane + TSH::TW + KP + 8 * i));
+  float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float re[4][4], im[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      tc::tmem_ld4(col + 8 * i + 4 * h, re[i]);
+      tc::tmem_ld4(col + TSH::N + 8 * i + 4 * h, im[i]);
+    }
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const float2 a0 = make_float2(re[0][l], im[0][l]);
+      const float2 a1 = cmul(make_float2(re[1][l], im[1][l]), w[0]);
+      const float2 a2 = cmul(make_float2(re[2][l], im[2][l]), w[1]);
+      const float2 a3 = cmul(make_float2(re[3][l], im[3][l]), w[2]);
+      const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = csub(a1, a3);
+      const float2 u0 = cadd(s02, s13), u2 = csub(s02, s13);
+      const float2 u1 = make_float2(d02.x - d13.y, d02.y + d13.x), u3 = make_float2(d02.x + d13.y, d02.y - d13.x);
+      e[0] = fmaf(u0.x, u0.x, fmaf(u0.y, u0.y, e[0]));
+      e[1] = fmaf(u1.x, u1.x, fmaf(u1.y, u1.y, e[1]));
+      e[2] = fmaf(u2.x, u2.x, fmaf(u2.y, u2.y, e[2]));
+      e[3] = fmaf(u3.x, u3.x, fmaf(u3.y, u3.y, e[3]));
+    }
+  }
+  const float emax = fmaxf(fmaxf(e[0], e[1]), fmaxf(e[2], e[3]));
+  return __all_sync(0xffffffffu, !active || emax < thr);
 }
 
 // One tile (TR lines of one snapshot) of the specialised rows pass, complex64 band engine,
@@ -1143,8 +1199,19 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   // flags and the state when PDL releases this grid, so everything waits first.
   constexpr bool PRE_WAIT_READS = KP2 == 0;
   if constexpr (!PRE_WAIT_READS) pdl_wait();
-  const unsigned fl = ZS ? __ldcg(fw) : 0xffffffffu;
-  const unsigned u_maybe_nonzero = ZS ? __ldcg(tword) : 1u;
+  unsigned fl = 0xffffffffu, u_maybe_nonzero = 1u;
+  if constexpr (TCI) {                 // prefetched during the CTA's previous tile
+    if (tci->pre) {
+      fl = tci->pfl;
+      u_maybe_nonzero = tci->ptw;
+    } else {
+      fl = __ldcg(fw);
+      u_maybe_nonzero = __ldcg(tword);
+    }
+  } else if constexpr (ZS) {
+    fl = __ldcg(fw);
+    u_maybe_nonzero = __ldcg(tword);
+  }
   bool warp_zero = false;   // the whole warp's next operator input is zero
   float2 a[KP];
   __shared__ unsigned live_rows[(TR + 31) / 32];   // lines whose next operator input is nonzero
@@ -1164,18 +1231,25 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   }
   if constexpr (PRE_WAIT_READS) pdl_wait();
   if (G.do_inv) {
+    // Level-1 register IDFT.  With zero-segment flags (ZS) and KP >= 16 it is the screened
+    // variant: residue classes of outputs whose Parseval energy bound lies below the threshold
+    // for the whole warp skip their sub-DFT and per-point tests (band_fft.cuh).
+    constexpr bool SCREEN = ZS && (KP == 16 || KP == 32);
+    unsigned pass = 0u;
+    const float thr_scale = G.screen ? (1.0f - 1.0f / 1024.0f) / (float)(KP / 4) : -1.0f;
+    bool ez = false;          // TMEM energy screen: the whole warp provably stays zero
+    constexpr bool ONE = TR * K == NT;     // tensor-core tiles with one band value per thread: prefetched
     if constexpr (TCI) {
-      // pipelined tensor-core level 2: this tile's MMA is in flight (issued during the previous
-      // tile); stage the NEXT tile's band V[b'][k][l2' + i] into the other B buffer (tf32 hi/lo)
-      if (tci->next >= 0) {
-        const int nrow0 = tci->next * TR;
-        const int nb = nrow0 / L2;
-        const long long nvbase = (long long)nb * K * L2 + (nrow0 - nb * L2);
+      // tensor-core level 2: this tile's band V[b][k][l20 + i] -> B tiles (tf32 hi/lo)
+      if (ONE && tci->pre) {
+        tc_put_b<KP, MO, TR>(tci->Bt, tid / TR, tid % TR, tci->pv);
+      } else {
         for (int idx = tid; idx < TR * K; idx += NT) {
           const int k = idx / TR, i2 = idx % TR;
-          tc_put_b<KP, MO, TR>(tci->Bt[tci->buf ^ 1], k, i2, __ldcg(io.V + nvbase + (long long)k * L2 + i2));
+          tc_put_b<KP, MO, TR>(tci->Bt, k, i2, __ldcg(io.V + vbase + (long long)k * L2 + i2));
         }
       }
+      tc::fence_async_smem();   // B writes -> visible to the tensor core
     } else {
       // band tile V[b][k][l20 + ii] -> Xs[ii][k]
       for (int idx = tid; idx < TR * K; idx += NT) {
@@ -1188,20 +1262,37 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
     }
     if (G.do_fwd && tid < (TR + 31) / 32) live_rows_zero(tid);
-    if constexpr (TCI) {
-      // ---- band inverse, level 2 of this tile from TMEM (times the level-1 twiddle); every
-      // thread's D reads and B writes precede the barrier, after which the next MMA is issued
-      tc_read<KP, MO, TR>(*tci, ii, a);
-      tc::fence_async_smem();   // B writes -> visible to the tensor core
-    }
     __syncthreads();
-    if constexpr (TCI) {
-      if (tid == 0 && tci->next >= 0) tc_issue<KP, MO, TR>(*tci, tci->Bt[tci->buf ^ 1]);
-      tci->buf ^= 1;
-    }
     unsigned nfl = 0;
     float l1 = 0.f;           // fused objective: sum of |c_{t+1}| over this thread's updated points
-    if constexpr (TCI) reg_dft<KP, true>(a);   // level-1 register IDFT
+    if constexpr (TCI) {
+      if (tid == 0) tc_issue<KP, MO, TR>(*tci);
+      // while the MMAs run: the next tile's flag words and this thread's band value of it
+      tci->pre = 0;
+      if (tci->next >= 0) {
+        const int nrow0 = tci->next * TR;
+        const int nb = nrow0 / L2;
+        if constexpr (ZS) {
+          tci->pfl = __ldcg(flags + ((long long)tci->next * (NT / 32 + 1) + (tid >> 5)));
+          tci->ptw = __ldcg(flags + ((long long)tci->next * (NT / 32 + 1) + NT / 32));
+        }
+        if constexpr (ONE)
+          tci->pv = __ldcg(io.V + (long long)nb * K * L2 + (nrow0 - nb * L2) + (long long)(tid / TR) * L2 + tid % TR);
+        tci->pre = 1;
+      }
+      // ---- band inverse, level 2 of this tile from TMEM (times the level-1 twiddle)
+      tc_wait(*tci);
+      if constexpr (SCREEN && KP == 32) {
+        if (fl == 0u && G.screen)
+          ez = tc_energy_screen<KP, MO, TR>(*tci, ii, kap2_lo * thr_scale, active);
+      }
+      if (!ez) {
+        tc_read<KP, MO, TR>(*tci, ii, a);
+        if constexpr (SCREEN) pass = reg_idft_screened<KP>(a, kap2_lo, thr_scale, fl, active);
+        else reg_dft<KP, true>(a);
+      }
+      tc::fence_before_sync();   // these TMEM reads precede the next tile's MMAs (barrier between)
+    }
     {
       // ---- band inverse (level 2 broadcast + twiddle, level 1 register IDFT); the band row
       // is read as 16-byte pairs
@@ -1225,7 +1316,8 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       }
 #pragma unroll
       for (int j = 0; j < KP; ++j) a[j] = cmulc(a[j], tw1s[j * R + s]);
-      reg_dft<KP, true>(a);
+      if constexpr (SCREEN) pass = reg_idft_screened<KP>(a, kap2_lo, thr_scale, fl, active);
+      else reg_dft<KP, true>(a);
       }
       // ---- fused epilogue, register-pipelined state stream.
       // Warp-level fast path: a clear segment whose 32 points all stay below the threshold
@@ -1233,11 +1325,12 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       // covers all KP segments; when every segment qualifies the loop is skipped.
       unsigned fast = 0u;
       if constexpr (ZS) {
-        unsigned pass = 0u;
+        if constexpr (!SCREEN) {
 #pragma unroll
-        for (int r = 0; r < KP; ++r) pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+          for (int r = 0; r < KP; ++r) pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+        }
         if (!active) pass = 0xffffffffu;
-        fast = __reduce_and_sync(0xffffffffu, pass) & ~fl;
+        fast = ez ? 0xffffffffu : (__reduce_and_sync(0xffffffffu, pass) & ~fl);
       }
       constexpr unsigned ALL = KP >= 32 ? 0xffffffffu : ((1u << KP) - 1u);
       if (ZS && (fast & ALL) == ALL) {
@@ -1280,7 +1373,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
         }
       }
     }
-    if (ZS && lane == 0) *fw = nfl;
+    if (ZS && lane == 0 && (nfl | fl)) *fw = nfl;   // (a clear word stays clear: no store)
     if constexpr (TRACE) {   // whole CTA in one snapshot: one atomic per warp
       double v = (double)l1;
 #pragma unroll
@@ -1416,11 +1509,10 @@ __global__ void __launch_bounds__(256, MINB)
   __shared__ uint32_t tmem_base;
   TcInv t;
   t.At = smem_raw + off;
-  t.Bt[0] = t.At + TSH::A_BYTES;
-  t.Bt[1] = t.Bt[0] + TSH::B_BYTES;
+  t.Bt = t.At + TSH::A_BYTES;
   t.mbar = &mbar;
   t.phase = 0;
-  t.buf = 0;
+  t.pre = 0;
   tc_stage_a<MO>(t.At, threadIdx.x, TS::NT);
   if (threadIdx.x == 0) {
     tc::mbar_init(&mbar, 1);
@@ -1437,28 +1529,16 @@ __global__ void __launch_bounds__(256, MINB)
   __syncthreads();
   tc::fence_after_sync();
   const FusedCols nofc{};
-  if (G.do_inv && (int)blockIdx.x < ntiles) {
-    // pipeline prologue: the first tile's band -> B[0], its MMA in flight
-    pdl_wait();
-    const int row0 = blockIdx.x * TS::TR;
-    const int b = row0 / G.L2;
-    const long long vbase = (long long)b * TS::K * G.L2 + (row0 - b * G.L2);
-    for (int idx = threadIdx.x; idx < TS::TR * TS::K; idx += TS::NT) {
-      const int k = idx / TS::TR, i2 = idx % TS::TR;
-      tc_put_b<KP, MO, TS::TR>(t.Bt[0], k, i2, __ldcg(io.V + vbase + (long long)k * G.L2 + i2));
-    }
-    tc::fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) tc_issue<KP, MO, TS::TR>(t, t.Bt[0]);
-  }
   // No barrier between tiles: the next tile writes shared memory only after barriers every
-  // thread passes after its last read of it here (B is double-buffered; live_rows, Xs and S
-  // are last read before this tile's final __syncthreads), and its MMA overwrites D only after
-  // the barrier that follows every thread's TMEM read.
+  // thread passes after its last read of it here (B is rewritten after every thread's mbarrier
+  // wait of this tile; live_rows, Xs and S are last read before this tile's final
+  // __syncthreads), and its MMAs overwrite D only after the barrier that follows every
+  // thread's TMEM reads.
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     t.next = tile + (int)gridDim.x < ntiles ? tile + (int)gridDim.x : -1;
     rows_tile<KP, R, MO, FistaPolicy<MOM>, true, 0, true, TRACE>(G, ax, io, epi, flags, nofc, tile, tw1s, tw2s, Xs,
                                                                  &t);
+    if (G.dbg & 1) __syncthreads();
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -1679,7 +1759,7 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : 2)
       }
       a[r] = make_double2(zn.x - vn.x, zn.y - vn.y);
     }
-    if (ZS && lane == 0) *fw = nfl;
+    if (ZS && lane == 0 && (nfl | fl)) *fw = nfl;   // (a clear word stays clear: no store)
   } else if (active) {
 #pragma unroll
     for (int r = 0; r < KP; ++r) {

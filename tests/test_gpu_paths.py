@@ -343,3 +343,29 @@ def test_tensor_core_rows_engine_matches_cuda_core_engine(tmp_path, cfg, nsnap, 
         assert e_tc < 1e-5 and e_cc < 1e-5, (e_tc, e_cc)
         assert orc.rel_l2(outs[0][s_], outs[1][s_]) < 1e-5
         np.testing.assert_array_equal(orc.topk(outs[0][s_], w.targets), orc.topk(ref, w.targets))
+
+
+@pytest.mark.parametrize("cfg,solver,nsnap,iters", [(2, "fista", 9, 200), (3, "admm", 3, 120), (4, "fista", 3, 150),
+                                                    (5, "fista", 1, 60), (5, "ista", 1, 40)])
+def test_energy_screen_is_bitwise_neutral(tmp_path, cfg, solver, nsnap, iters):
+    """The energy screen of the level-1 inverse register DFT (band_fft.cuh reg_idft_screened:
+    residue classes whose Parseval bound lies below the soft threshold for the whole warp skip
+    their sub-DFT and per-point tests) only skips points that provably stay exactly zero:
+    BCCB_SCREEN=0 (every class computed, same arithmetic) must give the same bits (fresh
+    processes), and the iterate must have gone sparse so the screen really fires."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(_PDL_SCRIPT.replace("range(9)", f"range({nsnap})"))
+    outs = []
+    for env in ({}, {"BCCB_SCREEN": "0"}):
+        out = tmp_path / f"est{len(outs)}.npy"
+        subprocess.run([sys.executable, str(script), root, str(out), str(cfg), solver, str(iters)], check=True,
+                       env=dict(os.environ, **env), timeout=900)
+        outs.append(np.load(out))
+    assert np.isfinite(outs[0]).all() and np.count_nonzero(outs[0]) > 0
+    if solver != "admm":
+        assert np.count_nonzero(outs[0]) < 0.05 * outs[0].size
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -30,4 +30,5 @@ ncu -i $OUT/cfg5_rows_tc.ncu-rep --page source --csv --print-source=sass,cuda > 
 python tools/ncu_source_hot.py $OUT/cfg5_rows_tc_source.csv 40 > $OUT/cfg5_rows_tc_hot_lines.txt 2>/dev/null
 cp profiles/r2e_cfg5_rows_tc*.txt $OUT/ 2>/dev/null
 gzip -f $OUT/cfg5_rows_tc_source.csv
+rm -f $OUT/cfg5_rows_tc.ncu-rep   # (gpurun_out is capped at 64 MiB; the text summaries are kept)
 echo done
