@@ -266,7 +266,7 @@ def ncu_summary(cfg):
         return {}
 
 
-def build_roofline(w, T, B, value_per_gpu, rows_ms, n_rows, kern_ms_total, step_ms_total, cols, clk):
+def build_roofline(w, T, B, value_per_gpu, rows_ms, n_rows, kern_ms_total, step_ms_total, cols, clk, nsub=1):
     """Roofline of the dominant kernel (the rows pass), against the bound that binds.
 
     The band-pruned, sparsity-skipping rows pass is FP32-issue bound (profiles/: sm__throughput
@@ -290,11 +290,15 @@ def build_roofline(w, T, B, value_per_gpu, rows_ms, n_rows, kern_ms_total, step_
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "measured (MEASURED_PEAKS.json copy test)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    launch_s = rows_ms / 1e3
+    # nsub sub-batch streams run their launches concurrently: a launch's event-to-event duration
+    # then covers time shared with nsub - 1 other launches, so rates use the exclusive share
+    # rows_ms / nsub (the sum over all launches / nsub is the time the rows pass occupies a step)
+    launch_s = rows_ms / max(nsub, 1) / 1e3
     r = {"kernel": f"rows_{w.solver}_kernel (band IFFT + fused prox/momentum epilogue + band FFT)",
-         "avg_launch_ms": rows_ms, "launches_per_step": n_rows,
+         "avg_launch_ms": rows_ms, "avg_launch_ms_exclusive": rows_ms / max(nsub, 1),
+         "launches_per_step": n_rows,
          "gpi_per_launch": gpi_per_launch, "iterations_per_launch": iters_per_launch,
-         "share_of_step": kern_ms_total / step_ms_total if step_ms_total else None,
+         "share_of_step": kern_ms_total / max(nsub, 1) / step_ms_total if step_ms_total else None,
          "launch_timing": "CUDA events around every launch of the timed steps, on the launch's stream"}
     if flops_gpi:
         achieved = flops_gpi * gpi_per_launch / launch_s / 1e12
@@ -446,15 +450,18 @@ def main():
             cols = None
             if n_k[1]:
                 cols = {"kernel": "cols pass (band FFT . D + P.Bhat . band IFFT)", "avg_launch_ms": ms_k[1] / n_k[1],
-                        "launches_per_step": n_k[1], "share_of_step": ms_k[1] / prof_ms}
-            roofline = build_roofline(w, T, B, value / world, rows_ms, n_k[0], ms_k[0], prof_ms, cols, clk)
+                        "avg_launch_ms_exclusive": ms_k[1] / n_k[1] / max(nsub, 1),
+                        "launches_per_step": n_k[1], "share_of_step": ms_k[1] / max(nsub, 1) / prof_ms}
+            roofline = build_roofline(w, T, B, value / world, rows_ms, n_k[0], ms_k[0], prof_ms, cols, clk, nsub)
             roofline["substreams"] = nsub
             roofline["profiled_step_ms"] = prof_ms
             roofline["launch_timing"] = ("CUDA events around every launch of one extra step (same stream "
                                          "configuration as the timed steps), on the launch's stream")
             if nsub > 1:
-                roofline["launch_timing"] += (f"; {nsub} sub-batch streams run concurrently, so per-launch "
-                                              "durations include time shared with the other streams")
+                roofline["launch_timing"] += (f"; {nsub} sub-batch streams run concurrently, so a launch's "
+                                              "duration includes time shared with the other streams: rates "
+                                              "(achieved, hbm, issue) and share_of_step use duration / "
+                                              f"{nsub} (avg_launch_ms_exclusive)")
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None

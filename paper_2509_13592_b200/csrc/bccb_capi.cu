@@ -563,13 +563,15 @@ static const AxisPrec& rows_axis(const AxisHost& ax, bool tc = false) {
 }
 
 // threads per CTA of the specialised FISTA rows pass (flags: one 32-bit word per warp)
-static int zs_threads(const AxisHost& ax, bool tc = false) { return std::max(256, rows_axis(ax, tc).R); }
+static int zs_threads(const AxisHost& ax, bool tc = false) {
+  return tc ? tc_threads(ax.t.KP) : std::max(256, rows_axis(ax, tc).R);
+}
 static size_t zs_flag_bytes(const bccb_plan_s* p, int batch, bool tc = false);
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R, int extra_words = 0) {
-  const int nt = std::max(256, R);
+static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R, int extra_words = 0, int ntmin = 256) {
+  const int nt = std::max(ntmin, R);
   const int tr = nt / R;
   const long long rows = (long long)batch * p->L2;
   const long long ctas = (rows + tr - 1) / tr;
@@ -582,7 +584,7 @@ static size_t flag_bytes_for(const bccb_plan_s* p, int batch, int R, int extra_w
 static size_t zs_flag_bytes_d(const bccb_plan_s* p, int batch) { return flag_bytes_for(p, batch, p->ax1.d.R); }
 
 static size_t zs_flag_bytes(const bccb_plan_s* p, int batch, bool tc) {
-  return flag_bytes_for(p, batch, rows_axis(p->ax1, tc).R, 1);
+  return flag_bytes_for(p, batch, rows_axis(p->ax1, tc).R, 1, tc ? tc_threads(p->ax1.t.KP) : 256);
 }
 static size_t zs_flag_bytes_max(const bccb_plan_s* p, int batch) {
   size_t b = std::max(zs_flag_bytes(p, batch), zs_flag_bytes_d(p, batch));
@@ -707,6 +709,10 @@ static Geo rows_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool
   Geo G;
   G.screen = rows_screen_env() ? 1 : 0;
   G.dbg = debug_env();
+  if ((p->L2 & (p->L2 - 1)) == 0) {
+    G.l2_shift = 0;
+    while ((1 << G.l2_shift) < p->L2) ++G.l2_shift;
+  }
   G.L1 = p->L1;
   G.L2 = p->L2;
   G.rows = (long long)batch * p->L2;
@@ -908,10 +914,10 @@ static FusedCols make_fused(const bccb_plan_s* p, int batch, const Workspace& w,
 template <int KP, int MO, bool MOM, bool TRACE>
 static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float2>& ax, const RowsIO<float2>& io,
                            const EpiFista& epi, unsigned* fl, cudaStream_t st) {
-  using TS = TileShape<KP, 128, MO>;
+  using TS = TileShape<KP, 128, MO, tc_threads(KP)>;
   using TSH = TcShape<KP, MO, TS::TR>;
   // resident CTAs per SM the register budget targets: the KP-point register DFT dominates
-  constexpr int MINB = KP == 8 ? 4 : (KP == 16 ? 3 : 2);
+  constexpr int MINB = (KP == 8 ? 4 : (KP == 16 ? 3 : 2)) * (256 / tc_threads(KP));
   auto k = rows_fista_tc_kernel<KP, MO, MOM, MINB, TRACE>;
   size_t smem = (size_t)(TS::TR * TS::XP + TS::TR * TS::SP) * sizeof(float2);
   if (TS::STAGE_TW) smem += (size_t)(KP + MO) * 128 * sizeof(float2);
@@ -933,7 +939,7 @@ static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float
   const int ntiles = (int)((G.rows + TS::TR - 1) / TS::TR);
   const unsigned grid = (unsigned)std::min<long long>(ntiles, (long long)o * num_sms());
   LaunchShape sh;
-  sh.threads = 256;
+  sh.threads = TS::NT;
   sh.TR = TS::TR;
   sh.smem = smem;
   return launch_pass<float2>(k, KIND_ROWS, grid, sh, st, G, ax, io, epi, fl, ntiles);
@@ -942,8 +948,8 @@ static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float
 static int launch_rows_fista_tc(const bccb_plan_s* p, int batch, bool inv, bool fwd, const Workspace& w,
                                 const EpiFista& epi, cudaStream_t st) {
   LaunchShape sh;
-  sh.threads = 256;
-  sh.TR = 2;
+  sh.threads = tc_threads(p->ax1.t.KP);
+  sh.TR = sh.threads / 128;
   const Geo G = rows_geo(p, batch, sh, inv, fwd);
   RowsIO<float2> io{(const float2*)w.V, (float2*)w.U};
   const AxisT<float2> ax = p->ax1.dev_t();
@@ -1098,8 +1104,8 @@ static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace
                                 cudaStream_t st, bool tc = false) {
   LaunchShape sh = fast_shape(p);
   if (tc) {
-    sh.threads = 256;
-    sh.TR = 2;
+    sh.threads = tc_threads(p->ax1.t.KP);
+    sh.TR = sh.threads / 128;
   }
   const Geo G = rows_geo(p, batch, sh, false, false);
   sh.smem = 0;
@@ -1107,9 +1113,12 @@ static int launch_zero_segments(const bccb_plan_s* p, int batch, const Workspace
   const unsigned* fl = (const unsigned*)w.flags;
   if (tc) {
     const int kp = p->ax1.t.KP;
-    if (kp == 8) return launch_pass<float2>(zero_segments_kernel<8, 128, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
-    if (kp == 16) return launch_pass<float2>(zero_segments_kernel<16, 128, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
-    if (kp == 32) return launch_pass<float2>(zero_segments_kernel<32, 128, T2>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (kp == 8)
+      return launch_pass<float2>(zero_segments_kernel<8, 128, T2, tc_threads(8)>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (kp == 16)
+      return launch_pass<float2>(zero_segments_kernel<16, 128, T2, tc_threads(16)>, KIND_OTHER, grid, sh, st, G, c, d, fl);
+    if (kp == 32)
+      return launch_pass<float2>(zero_segments_kernel<32, 128, T2, tc_threads(32)>, KIND_OTHER, grid, sh, st, G, c, d, fl);
     return fail(BCCB_ERR_UNSUPPORTED, "no tensor-core zero-segment specialisation");
   }
   if (rows_use_kp16(p->ax1)) {

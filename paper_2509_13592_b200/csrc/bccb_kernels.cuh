@@ -39,6 +39,7 @@ struct Geo {
   int TR;          // lines per CTA
   int do_inv, do_fwd;
   int screen = 0;  // rows passes: energy-screened level-1 inverse DFT (BCCB_SCREEN, default on)
+  int l2_shift = -1;  // log2(L2) when L2 is a power of two (rows passes: snapshot of a line by shift)
   int dbg = 0;     // BCCB_DEBUG bits: 1 = barrier between tensor-core tiles, 2 = unsplit column sums
 };
 
@@ -756,9 +757,14 @@ struct FusedCols {
 // staged (short-latency LDS instead of L1 round trips, measured +1% at config 2); larger ones
 // are read through L1 (a 36 KB table at L1 = 4096 would cost a resident CTA per SM, measured
 // -18% at config 5).
-template <int KP, int R, int MO>
+// threads per CTA of the tensor-core rows tiles: two line teams.  Single-line tiles (128 threads,
+// 4 CTAs per SM, N = KP) measured slower at config 5, 284 vs 330 G gpi/s: the per-tile flag /
+// staging / MMA round trip is paid per line (profiles/r2/r2h_*).
+__host__ __device__ constexpr int tc_threads(int KP) { return 256; }
+
+template <int KP, int R, int MO, int NTMIN = 256>
 struct TileShape {
-  static constexpr int NT = R > 256 ? R : 256;   // threads per CTA
+  static constexpr int NT = R > NTMIN ? R : NTMIN;   // threads per CTA
   static constexpr int TR = NT / R;              // lines per CTA
   static constexpr int K = KP * MO;
   static constexpr int XP = K + 2;   // even: 16-byte aligned band rows (LDS.128 pairs)
@@ -1113,6 +1119,58 @@ __device__ __forceinline__ void tc_read(const TcInv& t, int ii, float2 (&a)[KP])
   }
 }
 
+// Second-level screen of one residue class q (warp-uniform) of the TMEM energy screen: the
+// class's eight first-stage values u[l] are formed again from TMEM, one more decimation-in-
+// frequency split gives the two 4-output sub-classes (even / odd p of x[4 p + q]) with the
+// Parseval bounds 4 sum_l' |u[l'] +- u[l' + 4] phi|^2, phi = tw[4] W_8^q the twiddle ratio of
+// slots l' + 4 and l' (unit-modulus common factors dropped).  `thr4` = threshold / 4.
+template <int KP, int MO, int TR>
+__device__ __forceinline__ bool tc_class_rescreen(const TcInv& t, int ii, int q, const float2 (&w)[3], float thr4,
+                                                  bool active) {
+  using TSH = TcShape<KP, MO, TR>;
+  const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
+  const uint32_t col = lane + (uint32_t)(ii * KP);
+  // i^q as (cq, sq); W_8^q = exp(+i pi q / 4)
+  const float cq = (q == 0) ? 1.f : ((q == 2) ? -1.f : 0.f);
+  const float sq = (q == 1) ? 1.f : ((q == 3) ? -1.f : 0.f);
+  const float r = 0.70710678118654752f;
+  const float2 w8 = (q == 0) ? make_float2(1.f, 0.f)
+                             : ((q == 1) ? make_float2(r, r) : ((q == 2) ? make_float2(0.f, 1.f) : make_float2(-r, r)));
+  const float2 phi = cmul(make_float2(tc::tmem_ld1(lane + TSH::TW + 4), tc::tmem_ld1(lane + TSH::TW + KP + 4)), w8);
+  float2 u[8];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float re[4][4], im[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      tc::tmem_ld4(col + 8 * i + 4 * h, re[i]);
+      tc::tmem_ld4(col + TSH::N + 8 * i + 4 * h, im[i]);
+    }
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const float2 a0 = make_float2(re[0][l], im[0][l]);
+      const float2 a1 = cmul(make_float2(re[1][l], im[1][l]), w[0]);
+      const float2 a2 = cmul(make_float2(re[2][l], im[2][l]), w[1]);
+      const float2 a3 = cmul(make_float2(re[3][l], im[3][l]), w[2]);
+      // u = a0 + i^q a1 + (-1)^q a2 + (-i)^q a3 = (a0 + (-1)^q a2) + i^q (a1 + (-1)^q a3)
+      const float sg = (q & 1) ? -1.f : 1.f;
+      const float2 p02 = make_float2(fmaf(sg, a2.x, a0.x), fmaf(sg, a2.y, a0.y));
+      const float2 p13 = make_float2(fmaf(sg, a3.x, a1.x), fmaf(sg, a3.y, a1.y));
+      u[4 * h + l] = make_float2(p02.x + cq * p13.x - sq * p13.y, p02.y + cq * p13.y + sq * p13.x);
+    }
+  }
+  float ee = 0.f, eo = 0.f;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const float2 v = cmul(u[l + 4], phi);
+    const float2 a = cadd(u[l], v), b = csub(u[l], v);
+    ee = fmaf(a.x, a.x, fmaf(a.y, a.y, ee));
+    eo = fmaf(b.x, b.x, fmaf(b.y, b.y, eo));
+  }
+  return __all_sync(0xffffffffu, !active || fmaxf(ee, eo) < thr4);
+}
+
 // Energy screen straight from TMEM (KP = 32; the thread's state is known to be all zero): the
 // radix-4 first stage of the screened inverse DFT (band_fft.cuh reg_idft_screened) on the
 // level-2 values Z[8 i + l], i < 4, without keeping any of them.  Only the energy of each residue
@@ -1156,8 +1214,16 @@ __device__ __forceinline__ bool tc_energy_screen(const TcInv& t, int ii, float t
       e[3] = fmaf(u3.x, u3.x, fmaf(u3.y, u3.y, e[3]));
     }
   }
-  const float emax = fmaxf(fmaxf(e[0], e[1]), fmaxf(e[2], e[3]));
-  return __all_sync(0xffffffffu, !active || emax < thr);
+  // classes whose bound fails somewhere in the warp get a second look (tc_class_rescreen)
+  unsigned ok = 0u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ok |= ((!active || e[q] < thr) ? 1u : 0u) << q;
+  ok = __reduce_and_sync(0xffffffffu, ok);
+  if (ok == 0xfu) return true;
+  bool all = true;
+  for (int q = 0; q < 4 && all; ++q)
+    if (!((ok >> q) & 1u)) all = tc_class_rescreen<KP, MO, TR>(t, ii, q, w, 2.0f * thr, active);
+  return all;
 }
 
 // One tile (TR lines of one snapshot) of the specialised rows pass, complex64 band engine,
@@ -1170,7 +1236,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
                                           const FusedCols& fc, int tile, const float2* tw1s, const float2* tw2s,
                                           float2* Xs, TcInv* tci = nullptr) {
   static_assert(!TCI || (R == 128 && KP2 == 0), "tensor-core tiles: R = 128, no fused column pass");
-  using TS = TileShape<KP, R, MO>;
+  using TS = TileShape<KP, R, MO, TCI ? tc_threads(KP) : 256>;
   using St = typename Pol::S;
   constexpr int NT = TS::NT, TR = TS::TR, K = TS::K, XP = TS::XP, PITCH = TS::PITCH, SP = TS::SP;
   constexpr int CH = 2;
@@ -1182,7 +1248,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   const int gr = row0 + ii;
   const bool active = gr < (int)G.rows;
   const int L2 = G.L2;
-  const int b = row0 / L2;                     // whole CTA lies in one snapshot
+  const int b = G.l2_shift >= 0 ? (row0 >> G.l2_shift) : row0 / L2;   // whole CTA lies in one snapshot
   const int l20 = row0 - b * L2;
   const long long vbase = (long long)b * K * L2 + l20;   // io.V/U index of (k=0, ii=0)
   const Pol pol(epi, (long long)gr * G.L1 + s, b);
@@ -1271,7 +1337,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       tci->pre = 0;
       if (tci->next >= 0) {
         const int nrow0 = tci->next * TR;
-        const int nb = nrow0 / L2;
+        const int nb = G.l2_shift >= 0 ? (nrow0 >> G.l2_shift) : nrow0 / L2;
         if constexpr (ZS) {
           tci->pfl = __ldcg(flags + ((long long)tci->next * (NT / 32 + 1) + (tid >> 5)));
           tci->ptw = __ldcg(flags + ((long long)tci->next * (NT / 32 + 1) + NT / 32));
@@ -1491,11 +1557,11 @@ __global__ void __launch_bounds__(R > 256 ? R : 256, R > 256 ? 1 : MINB)
 // of rows_tile is unchanged.  Persistent: each CTA stages the constant A tiles, allocates its
 // TMEM columns and initialises its mbarrier once, then walks tiles blockIdx.x, +gridDim.x, ...
 template <int KP, int MO, bool MOM, int MINB, bool TRACE = false>
-__global__ void __launch_bounds__(256, MINB)
+__global__ void __launch_bounds__(tc_threads(KP), MINB)
     rows_fista_tc_kernel(Geo G, AxisT<float2> ax, RowsIO<float2> io, EpiFista epi, unsigned* __restrict__ flags,
                          int ntiles) {
   constexpr int R = 128;
-  using TS = TileShape<KP, R, MO>;
+  using TS = TileShape<KP, R, MO, tc_threads(KP)>;
   using TSH = TcShape<KP, MO, TS::TR>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* Xs = reinterpret_cast<float2*>(smem_raw);
@@ -2105,11 +2171,11 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 1) cluster64_fi
 
 // Final pass of a zero-skipping run: write the zeros of every clear segment back so c (and d)
 // are dense, consistent arrays again.
-template <int KP, int R, typename T2 = float2>
-__global__ void __launch_bounds__(R > 256 ? R : 256) zero_segments_kernel(Geo G, double2* c, T2* d,
-                                                                          const unsigned* __restrict__ flags) {
+template <int KP, int R, typename T2 = float2, int NTMIN = 256>
+__global__ void __launch_bounds__(R > NTMIN ? R : NTMIN) zero_segments_kernel(Geo G, double2* c, T2* d,
+                                                                              const unsigned* __restrict__ flags) {
   pdl_wait();
-  constexpr int NT = R > 256 ? R : 256;
+  constexpr int NT = R > NTMIN ? R : NTMIN;
   constexpr int TR = NT / R;
   const int tid = threadIdx.x;
   const int ii = tid / R, s = tid % R;
