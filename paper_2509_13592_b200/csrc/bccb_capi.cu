@@ -687,8 +687,10 @@ static int prep_smem(KernelT kernel, size_t smem) {
     default: return fail(BCCB_ERR_UNSUPPORTED, "register DFT size %d", KPVAL);  \
   }
 
-// Energy screen of the level-1 inverse DFT in the zero-skipping rows passes (band_fft.cuh
-// reg_idft_screened): bitwise neutral; BCCB_SCREEN=0 computes every residue class.
+// Energy screen of the level-1 inverse DFT in the zero-skipping rows passes, bitwise neutral.
+// BCCB_SCREEN bits: 1 (default) = the register screen of the CUDA-core engines (band_fft.cuh
+// reg_idft_screened), 2 = the TMEM screen of the tensor-core tiles (tc_energy_screen); 0 computes
+// every residue class.
 static int rows_screen_env() {
   static const int v = [] {
     const char* e = getenv("BCCB_SCREEN");
@@ -707,7 +709,7 @@ static int debug_env() {
 
 static Geo rows_geo(const bccb_plan_s* p, int batch, const LaunchShape& sh, bool inv, bool fwd) {
   Geo G;
-  G.screen = rows_screen_env() ? 1 : 0;
+  G.screen = rows_screen_env();
   G.dbg = debug_env();
   if ((p->L2 & (p->L2 - 1)) == 0) {
     G.l2_shift = 0;
@@ -932,9 +934,27 @@ static int launch_tc_shape(const bccb_plan_s* p, const Geo& G, const AxisT<float
     if (rc) return rc;
     CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
-    o = std::min<int>(MINB, (int)((228 * 1024) / (smem + 1024)));
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, k));
+    const size_t per_cta = smem + fa.sharedSizeBytes + 1024;       // dynamic + static + reserved
+    o = std::min<int>(MINB, (int)((228 * 1024) / per_cta));
     o = std::min(o, 512 / TSH::COLS);
     if (o < 1) return fail(BCCB_ERR_UNSUPPORTED, "tensor-core rows pass does not fit one SM");
+    // The kernel spills a few loop-carried scalars (128-register budget): leave the L1 as much
+    // room as the resident CTAs allow instead of the maximum shared-memory split (the spill
+    // reloads were L2 round trips with a 28 KB L1, profiles/r2/r2j_*).  Keep the smaller split
+    // only if the occupancy API confirms the same number of resident CTAs.
+    if (!(debug_env() & 4)) {      // BCCB_DEBUG bit 4: keep the maximum shared-memory split (A/B)
+      const int want_kb = (int)((o * per_cta + 1023) / 1024);
+      const int pct = std::min(100, (want_kb * 100 + 227) / 228 + 1);
+      if (cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct) == cudaSuccess) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, TS::NT, smem) != cudaSuccess || n < o)
+          CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared));
+      }
+      (void)cudaGetLastError();
+    }
   }
   const int ntiles = (int)((G.rows + TS::TR - 1) / TS::TR);
   const unsigned grid = (unsigned)std::min<long long>(ntiles, (long long)o * num_sms());

@@ -38,9 +38,12 @@ struct Geo {
   long long rows;  // total lines in this launch
   int TR;          // lines per CTA
   int do_inv, do_fwd;
-  int screen = 0;  // rows passes: energy-screened level-1 inverse DFT (BCCB_SCREEN, default on)
+  int screen = 0;  // rows passes, BCCB_SCREEN bits: 1 = energy-screened register IDFT (CUDA-core
+                   // engines, default), 2 = TMEM energy screen of the tensor-core tiles (off by
+                   // default: a tile waits for its slowest warp, and a warp that fails the screen
+                   // runs screen + full path: 346 vs 358 G gpi/s at config 5, profiles/r2/r2l_*)
   int l2_shift = -1;  // log2(L2) when L2 is a power of two (rows passes: snapshot of a line by shift)
-  int dbg = 0;     // BCCB_DEBUG bits: 1 = barrier between tensor-core tiles, 2 = unsplit column sums
+  int dbg = 0;     // BCCB_DEBUG bits: 1 = barrier between tensor-core tiles, 2 = unsplit column sums (4: host, L1 split)
 };
 
 // ------------------------------------------------------------------ epilogues
@@ -805,10 +808,10 @@ struct FistaPolicy {
   float2* dp;
   FistaScalars sc;
   float bn;
-  __device__ __forceinline__ FistaPolicy(const EpiFista& e, long long off, int b) {
+  __device__ __forceinline__ FistaPolicy(const EpiFista& e, long long off, int b, const double* tau_pre = nullptr) {
     cp = e.c + off;
     dp = MOM ? e.d + off : nullptr;
-    sc = FistaScalars{e.kscale * e.tau[b], e.a, e.beta_cur, b, e.it, e.first_bad};
+    sc = FistaScalars{e.kscale * (tau_pre ? *tau_pre : e.tau[b]), e.a, e.beta_cur, b, e.it, e.first_bad};
     bn = (float)e.beta_next;
   }
   // fused objective: |c_{t+1}| of an updated point (float: summed over at most KP points per
@@ -953,6 +956,25 @@ __device__ __forceinline__ void trace_add(const EpiAdmmSplit&, int, double) {}
 // tile), one thread issues the MMAs, every thread waits on the mbarrier and reads its lane of D.
 // B and D are single-buffered: the next tile stages B only after every thread has waited for
 // this tile's MMAs, and issues its MMAs after a barrier that follows every thread's D reads.
+// per-thread asynchronous global -> shared copies (LDGSTS): nothing is held in registers while
+// the copy is in flight (a register prefetch gets spilled by the 128-register budget, and the
+// spill store then blocks on the load: profiles/r2/r2i_*)
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(tc::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(tc::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// a thread's prefetch slot for its CTA's next tile (written and read by that thread only)
+struct TcPrefetch {
+  float2 pv;           // the thread's band value of the tile
+  unsigned fl, tw;     // its warp's flag word, the tile word
+  double tau;          // tau of the tile's snapshot
+};
+
 struct TcInv {
   unsigned char* At;   // [MO/4][re_hi | re_lo | im_hi | im_lo][128 x 8 tf32] (K-major, 4 KB each)
   unsigned char* Bt;   // [MO/4][hi | lo][N x 8 tf32]
@@ -963,8 +985,8 @@ struct TcInv {
   // prefetched during the previous tile (pre != 0): this thread's band value of the tile and
   // the tile's flag words
   int pre;
-  float2 pv;
-  unsigned pfl, ptw;
+  TcPrefetch* slot;    // shared memory
+  float2 w8[3];        // this lane's level-1 twiddles tw[8], tw[16], tw[24] (KP = 32: TMEM energy screen)
 };
 
 template <int KP, int MO, int TR>
@@ -1185,10 +1207,7 @@ __device__ __forceinline__ bool tc_energy_screen(const TcInv& t, int ii, float t
   static_assert(KP == 32, "TMEM energy screen: KP = 32");
   const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
   const uint32_t col = lane + (uint32_t)(ii * KP);
-  float2 w[3];
-#pragma unroll
-  for (int i = 1; i < 4; ++i)
-    w[i - 1] = make_float2(tc::tmem_ld1(lane + TSH::TW + 8 * i), tc::tmem_ld1(lane + TSH::TW + KP + 8 * i));
+  const float2 w[3] = {t.w8[0], t.w8[1], t.w8[2]};
   float e[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -1226,6 +1245,14 @@ __device__ __forceinline__ bool tc_energy_screen(const TcInv& t, int ii, float t
   return all;
 }
 
+template <typename Pol, typename Args>
+__device__ __forceinline__ Pol make_policy(const Args& e, long long off, int b, const double* tau_pre) {
+  if constexpr (std::is_constructible<Pol, const Args&, long long, int, const double*>::value)
+    return Pol(e, off, b, tau_pre);
+  else
+    return Pol(e, off, b);
+}
+
 // One tile (TR lines of one snapshot) of the specialised rows pass, complex64 band engine,
 // state policy Pol.  `tile` indexes the tile (and its flag words); with KP2 > 0 and do_fwd,
 // the last tile of a snapshot to arrive runs that snapshot's column pass.  Streaming state /
@@ -1251,7 +1278,16 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   const int b = G.l2_shift >= 0 ? (row0 >> G.l2_shift) : row0 / L2;   // whole CTA lies in one snapshot
   const int l20 = row0 - b * L2;
   const long long vbase = (long long)b * K * L2 + l20;   // io.V/U index of (k=0, ii=0)
-  const Pol pol(epi, (long long)gr * G.L1 + s, b);
+  // tensor-core tiles: the flag words, the band value and tau of this tile were copied into the
+  // thread's shared-memory slot during the CTA's previous tile
+  const double* tau_pre = nullptr;
+  if constexpr (TCI) {
+    if (tci->pre) {
+      cp_async_wait_group0();
+      tau_pre = &tci->slot->tau;
+    }
+  }
+  const Pol pol = make_policy<Pol>(epi, (long long)gr * G.L1 + s, b, tau_pre);
   const double kap = pol.kap();
   const float kap2_lo = (float)(kap * kap) * (1.0f - 1.0f / 262144.0f);
   const int lane = tid & 31;
@@ -1268,8 +1304,8 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
   unsigned fl = 0xffffffffu, u_maybe_nonzero = 1u;
   if constexpr (TCI) {                 // prefetched during the CTA's previous tile
     if (tci->pre) {
-      fl = tci->pfl;
-      u_maybe_nonzero = tci->ptw;
+      fl = tci->slot->fl;
+      u_maybe_nonzero = tci->slot->tw;
     } else {
       fl = __ldcg(fw);
       u_maybe_nonzero = __ldcg(tword);
@@ -1300,15 +1336,19 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     // Level-1 register IDFT.  With zero-segment flags (ZS) and KP >= 16 it is the screened
     // variant: residue classes of outputs whose Parseval energy bound lies below the threshold
     // for the whole warp skip their sub-DFT and per-point tests (band_fft.cuh).
-    constexpr bool SCREEN = ZS && (KP == 16 || KP == 32);
+    // (tensor-core tiles screen from TMEM instead and keep the plain register DFT for the warps
+    // that fail it: the screened register variant measured slower there, 300 vs 365 G gpi/s
+    // with every class computed, profiles/r2/r2g_bench_cfg5_screen0.json vs r2d)
+    constexpr bool SCREEN = ZS && !TCI && (KP == 16 || KP == 32);
+    constexpr bool TSCREEN = ZS && TCI && KP == 32;
     unsigned pass = 0u;
-    const float thr_scale = G.screen ? (1.0f - 1.0f / 1024.0f) / (float)(KP / 4) : -1.0f;
+    const float thr_scale = (G.screen & 1) ? (1.0f - 1.0f / 1024.0f) / (float)(KP / 4) : -1.0f;
     bool ez = false;          // TMEM energy screen: the whole warp provably stays zero
     constexpr bool ONE = TR * K == NT;     // tensor-core tiles with one band value per thread: prefetched
     if constexpr (TCI) {
       // tensor-core level 2: this tile's band V[b][k][l20 + i] -> B tiles (tf32 hi/lo)
       if (ONE && tci->pre) {
-        tc_put_b<KP, MO, TR>(tci->Bt, tid / TR, tid % TR, tci->pv);
+        tc_put_b<KP, MO, TR>(tci->Bt, tid / TR, tid % TR, tci->slot->pv);
       } else {
         for (int idx = tid; idx < TR * K; idx += NT) {
           const int k = idx / TR, i2 = idx % TR;
@@ -1338,24 +1378,25 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       if (tci->next >= 0) {
         const int nrow0 = tci->next * TR;
         const int nb = G.l2_shift >= 0 ? (nrow0 >> G.l2_shift) : nrow0 / L2;
-        if constexpr (ZS) {
-          tci->pfl = __ldcg(flags + ((long long)tci->next * (NT / 32 + 1) + (tid >> 5)));
-          tci->ptw = __ldcg(flags + ((long long)tci->next * (NT / 32 + 1) + NT / 32));
-        }
+        static_assert(ZS, "tensor-core tiles run with zero-segment flags");
+        cp_async4(&tci->slot->fl, flags + ((long long)tci->next * (NT / 32 + 1) + (tid >> 5)));
+        cp_async4(&tci->slot->tw, flags + ((long long)tci->next * (NT / 32 + 1) + NT / 32));
+        cp_async8(&tci->slot->tau, epi.tau + nb);
         if constexpr (ONE)
-          tci->pv = __ldcg(io.V + (long long)nb * K * L2 + (nrow0 - nb * L2) + (long long)(tid / TR) * L2 + tid % TR);
+          cp_async8(&tci->slot->pv,
+                    io.V + (long long)nb * K * L2 + (nrow0 - nb * L2) + (long long)(tid / TR) * L2 + tid % TR);
+        cp_async_commit_group();
         tci->pre = 1;
       }
       // ---- band inverse, level 2 of this tile from TMEM (times the level-1 twiddle)
       tc_wait(*tci);
-      if constexpr (SCREEN && KP == 32) {
-        if (fl == 0u && G.screen)
-          ez = tc_energy_screen<KP, MO, TR>(*tci, ii, kap2_lo * thr_scale, active);
+      if constexpr (TSCREEN) {
+        if (fl == 0u && (G.screen & 2))
+          ez = tc_energy_screen<KP, MO, TR>(*tci, ii, kap2_lo * (1.0f - 1.0f / 1024.0f) / (float)(KP / 4), active);
       }
       if (!ez) {
         tc_read<KP, MO, TR>(*tci, ii, a);
-        if constexpr (SCREEN) pass = reg_idft_screened<KP>(a, kap2_lo, thr_scale, fl, active);
-        else reg_dft<KP, true>(a);
+        reg_dft<KP, true>(a);
       }
       tc::fence_before_sync();   // these TMEM reads precede the next tile's MMAs (barrier between)
     }
@@ -1391,18 +1432,20 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       // covers all KP segments; when every segment qualifies the loop is skipped.
       unsigned fast = 0u;
       if constexpr (ZS) {
-        if constexpr (!SCREEN) {
+        if (ez) {
+          fast = 0xffffffffu;
+        } else {
+          if constexpr (!SCREEN) {
 #pragma unroll
-          for (int r = 0; r < KP; ++r) pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+            for (int r = 0; r < KP; ++r) pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+          }
+          if (!active) pass = 0xffffffffu;
+          fast = __reduce_and_sync(0xffffffffu, pass) & ~fl;
         }
-        if (!active) pass = 0xffffffffu;
-        fast = ez ? 0xffffffffu : (__reduce_and_sync(0xffffffffu, pass) & ~fl);
       }
       constexpr unsigned ALL = KP >= 32 ? 0xffffffffu : ((1u << KP) - 1u);
       if (ZS && (fast & ALL) == ALL) {
-#pragma unroll
-        for (int r = 0; r < KP; ++r) a[r] = make_float2(0.f, 0.f);
-        warp_zero = true;
+        warp_zero = true;   // a[] is not used again (the forward part writes zeros for this warp)
       } else
 #pragma unroll
       for (int r0 = 0; r0 < KP; r0 += CH) {
@@ -1483,7 +1526,11 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     }
   } else {
     const bool my_live = (live_rows[ii >> 5] >> (ii & 31)) & 1u;
-    if (active && my_live) {
+    if (active && my_live && warp_zero) {    // this warp's slice of a live line is zero
+      float2* Srow = S + ii * SP;
+#pragma unroll
+      for (int j = 0; j < KP; ++j) Srow[j * PITCH + s] = make_float2(0.f, 0.f);
+    } else if (active && my_live) {
       reg_dft<KP, false>(a);
       float2* Srow = S + ii * SP;
       if constexpr (TCI) {     // warp-uniform branch (a warp lies in one line): TMEM twiddles
@@ -1573,7 +1620,9 @@ __global__ void __launch_bounds__(tc_threads(KP), MINB)
   off = (off + 127) & ~(size_t)127;
   __shared__ uint64_t mbar;
   __shared__ uint32_t tmem_base;
+  __shared__ TcPrefetch prefetch_slots[TS::NT];
   TcInv t;
+  t.slot = &prefetch_slots[threadIdx.x];
   t.At = smem_raw + off;
   t.Bt = t.At + TSH::A_BYTES;
   t.mbar = &mbar;
@@ -1594,6 +1643,13 @@ __global__ void __launch_bounds__(tc_threads(KP), MINB)
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  if constexpr (KP == 32) {
+    const uint32_t lane = t.tmem + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+      t.w8[i - 1] = make_float2(tc::tmem_ld1(lane + TSH::TW + 8 * i), tc::tmem_ld1(lane + TSH::TW + KP + 8 * i));
+    tc::tmem_ld_wait();
+  }
   const FusedCols nofc{};
   // No barrier between tiles: the next tile writes shared memory only after barriers every
   // thread passes after its last read of it here (B is rewritten after every thread's mbarrier

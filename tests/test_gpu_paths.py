@@ -350,9 +350,10 @@ def test_tensor_core_rows_engine_matches_cuda_core_engine(tmp_path, cfg, nsnap, 
 def test_energy_screen_is_bitwise_neutral(tmp_path, cfg, solver, nsnap, iters):
     """The energy screen of the level-1 inverse register DFT (band_fft.cuh reg_idft_screened:
     residue classes whose Parseval bound lies below the soft threshold for the whole warp skip
-    their sub-DFT and per-point tests) only skips points that provably stay exactly zero:
-    BCCB_SCREEN=0 (every class computed, same arithmetic) must give the same bits (fresh
-    processes), and the iterate must have gone sparse so the screen really fires."""
+    their sub-DFT and per-point tests; on tensor-core tiles the two-level screen straight from
+    TMEM) only skips points that provably stay exactly zero: BCCB_SCREEN=0 (every class computed)
+    must give the same bits as both screens on (fresh processes), and the iterate must have gone
+    sparse so the screens really fire."""
     import os
     import subprocess
     import sys
@@ -360,7 +361,8 @@ def test_energy_screen_is_bitwise_neutral(tmp_path, cfg, solver, nsnap, iters):
     script = tmp_path / "run.py"
     script.write_text(_PDL_SCRIPT.replace("range(9)", f"range({nsnap})"))
     outs = []
-    for env in ({}, {"BCCB_SCREEN": "0"}):
+    # config 5 runs the tensor-core engine: its TMEM screen is bit 2 (off by default)
+    for env in ({"BCCB_SCREEN": "3"}, {"BCCB_SCREEN": "0"}):
         out = tmp_path / f"est{len(outs)}.npy"
         subprocess.run([sys.executable, str(script), root, str(out), str(cfg), solver, str(iters)], check=True,
                        env=dict(os.environ, **env), timeout=900)
