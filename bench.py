@@ -312,6 +312,14 @@ def build_roofline(w, T, B, value_per_gpu, rows_ms, n_rows, kern_ms_total, step_
     else:
         r.update({"bound": "fp32", "achieved": None, "peak": fp32_peak, "unit": "TFLOP/s", "frac": None,
                   "flops_source": "profiles/ncu_summary.json has no FP32 count for this config"})
+    if summ.get("late_phase_fp32_tflops_ncu"):
+        # the same kernel timed ALONE by ncu (serialised, cold cache): the lower bracket of the
+        # fraction; the live figure above credits the overlap of the concurrent sub-batch streams
+        r["ncu_alone"] = {"late_phase_fp32_tflops": summ["late_phase_fp32_tflops_ncu"],
+                          "frac": summ["late_phase_fp32_tflops_ncu"] / fp32_peak,
+                          "mean_launch_us": summ.get("rows_mean_us_ncu"),
+                          "mean_fp32_tflops": (flops_gpi * gpi_per_launch / (summ["rows_mean_us_ncu"] * 1e-6) / 1e12
+                                               if flops_gpi and summ.get("rows_mean_us_ncu") else None)}
     r["traffic"] = dram_gpi * gpi_per_launch if dram_gpi is not None else None
     r["traffic_note"] = "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (full-solve average)"
     if inst_gpi:

@@ -1,5 +1,5 @@
 """Config-5 snapshot trajectory: GPU FISTA after T iterations against float64 oracle iterates
-(tools/data/cfg5_snaps_s0.npz, made in the build container by running oracle.fista on the golden
+(tests/golden/cfg5_trajectory.npz, made in the build container by running oracle.fista on the golden
 measurements of tests/golden/cfg5_t1000.npz) — where along the 1000 iterations the fp32 engine
 drifts from the float64 trajectory."""
 import os, sys, json
@@ -10,7 +10,7 @@ from paper_2509_13592_b200 import scenes
 
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 g = np.load(os.path.join(root, "tests/golden/cfg5_t1000.npz"))
-sn = np.load(os.path.join(root, "tools/data/cfg5_snaps_s0.npz"))
+sn = np.load(os.path.join(root, "tests/golden/cfg5_trajectory.npz"))
 w = scenes.workload(5)
 geom = scenes.geometry_for(w)
 op = bb.gram_operator(geom, w.l1, w.l2)

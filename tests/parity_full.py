@@ -2,7 +2,7 @@
 and iteration count through the public API, with a sample of snapshots re-solved by the pinned
 float64 CPU oracle (oracle/bccb_oracle.py) in a process pool on the host cores.
 
-    python tools/parity_full.py OUT.json [--cfg5-iterations T] [--only 2,5]
+    python tests/parity_full.py OUT.json [--cfg5-iterations T] [--only 2,5]
 
 Writes rel-L2 (GPU estimate vs oracle) and top-K index-set agreement per checked snapshot.
 Config 3 compares c and v (the reference's z is identically zero there, SURVEY finding 7).

@@ -3,7 +3,7 @@ set -x
 OUT=gpurun_out/r2h
 mkdir -p $OUT
 timeout 900 python -m pytest tests/test_gpu_paths.py tests/test_gpu_tc.py -q -x --timeout 600 -k "screen or tensor_core or tf32 or substream" > $OUT/pytest_quick.log 2>&1; echo "rc=$?" >> $OUT/pytest_quick.log
-timeout 300 python tools/cfg5_trajectory.py $OUT/traj.json > $OUT/traj.log 2>&1
+timeout 300 python tests/cfg5_trajectory_tool.py $OUT/traj.json > $OUT/traj.log 2>&1
 timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 > $OUT/bench_cfg5.json 2>> $OUT/bench.err
 timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --substreams 1 > $OUT/bench_cfg5_sub1.json 2>> $OUT/bench.err
 timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --substreams 2 > $OUT/bench_cfg5_sub2.json 2>> $OUT/bench.err

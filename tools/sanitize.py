@@ -20,8 +20,14 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2509_13592_b200 as bb  # noqa: E402
-from oracle import bccb_oracle as orc  # noqa: E402
 from paper_2509_13592_b200 import scenes  # noqa: E402
+
+
+def adjoint(m1, m2, l1, l2, y):
+    """b = A^H y as L1 L2 ifft2 of the signed scatter of y (host numpy; inputs only)."""
+    e = np.zeros((l2, l1), dtype=np.complex128)
+    np.add.at(e, (np.asarray(m2) % l2, np.asarray(m1) % l1), y * (-1.0) ** (np.asarray(m1) + np.asarray(m2)))
+    return np.fft.ifft2(e).ravel() * (l1 * l2)
 
 
 def problem(cfg, nsnap, l1=None, l2=None):
@@ -30,7 +36,7 @@ def problem(cfg, nsnap, l1=None, l2=None):
     l1, l2 = l1 or w.l1, l2 or w.l2
     op = bb.gram_operator(geom, l1, l2)
     m1, m2 = geom.occupied_coordinates()
-    bs = np.stack([orc.adjoint_fft(m1, m2, l1, l2, y) for y in ys])
+    bs = np.stack([adjoint(m1, m2, l1, l2, y) for y in ys])
     taus = np.array([w.tau_fraction * np.abs(b).max() for b in bs])
     return w, op, ys, bs, taus
 
