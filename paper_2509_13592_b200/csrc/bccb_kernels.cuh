@@ -43,7 +43,7 @@ struct Geo {
                    // default: a tile waits for its slowest warp, and a warp that fails the screen
                    // runs screen + full path: 346 vs 358 G gpi/s at config 5, profiles/r2/r2l_*)
   int l2_shift = -1;  // log2(L2) when L2 is a power of two (rows passes: snapshot of a line by shift)
-  int dbg = 0;     // BCCB_DEBUG bits: 1 = barrier between tensor-core tiles, 2 = unsplit column sums (4: host, L1 split)
+  int dbg = 0;     // BCCB_DEBUG bits: 1 = barrier between tensor-core tiles, 2 = unsplit column sums (4: host, L1 split; 8/16/32/64: timing probes of the TC tile, results invalid)
 };
 
 // ------------------------------------------------------------------ epilogues
@@ -1372,7 +1372,7 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     unsigned nfl = 0;
     float l1 = 0.f;           // fused objective: sum of |c_{t+1}| over this thread's updated points
     if constexpr (TCI) {
-      if (tid == 0) tc_issue<KP, MO, TR>(*tci);
+      if (tid == 0 && !(G.dbg & 32)) tc_issue<KP, MO, TR>(*tci);
       // while the MMAs run: the next tile's flag words and this thread's band value of it
       tci->pre = 0;
       if (tci->next >= 0) {
@@ -1389,7 +1389,8 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
         tci->pre = 1;
       }
       // ---- band inverse, level 2 of this tile from TMEM (times the level-1 twiddle)
-      tc_wait(*tci);
+      if (!(G.dbg & (16 | 32))) tc_wait(*tci);
+      if (G.dbg & 64) ez = fl == 0u;     // timing probe only: no TMEM reads, no transform
       if constexpr (TSCREEN) {
         if (fl == 0u && (G.screen & 2))
           ez = tc_energy_screen<KP, MO, TR>(*tci, ii, kap2_lo * (1.0f - 1.0f / 1024.0f) / (float)(KP / 4), active);
@@ -1500,6 +1501,9 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
     }
   }
   if (!G.do_fwd) return;
+  if constexpr (TCI) {
+    if (G.dbg & 8) return;               // timing probe only: no forward part, no tile barrier
+  }
   // ---- band forward: register DFT, twiddle + transpose scatter, R-term reductions.
   // A line whose next operator input is entirely zero (most lines once the iterate is sparse)
   // has a zero band: its DFT, scatter and reductions are skipped.
