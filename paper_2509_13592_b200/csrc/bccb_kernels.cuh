@@ -1364,8 +1364,13 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
       }
     }
     if (!EARLY) {
+      if (fl & ((1u << CH) - 1u)) {          // warp-uniform: a clear flag word loads nothing
 #pragma unroll
-      for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
+        for (int q = 0; q < CH; ++q) sb[q] = pol.load(q * R, active && ((fl >> q) & 1u));
+      } else {
+#pragma unroll
+        for (int q = 0; q < CH; ++q) sb[q] = Pol::empty();
+      }
     }
     if (G.do_fwd && tid < (TR + 31) / 32) live_rows_zero(tid);
     __syncthreads();
@@ -1437,8 +1442,19 @@ __device__ __forceinline__ void rows_tile(const Geo& G, const AxisT<float2>& ax,
           fast = 0xffffffffu;
         } else {
           if constexpr (!SCREEN) {
+            // one predicate chain and one vote first: when every point of the warp is below the
+            // threshold (nearly all warps once the iterate is sparse) the per-slot bits are all
+            // ones (a NaN compares false, so it still reaches the per-slot path and the slow path)
+            bool below = true;
 #pragma unroll
-            for (int r = 0; r < KP; ++r) pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+            for (int r = 0; r < KP; ++r) below = below & (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo);
+            if (__all_sync(0xffffffffu, !active || below)) {
+              pass = 0xffffffffu;
+            } else {
+#pragma unroll
+              for (int r = 0; r < KP; ++r)
+                pass |= (fmaf(a[r].x, a[r].x, a[r].y * a[r].y) < kap2_lo ? 1u : 0u) << r;
+            }
           }
           if (!active) pass = 0xffffffffu;
           fast = __reduce_and_sync(0xffffffffu, pass) & ~fl;
